@@ -1,0 +1,164 @@
+/* wcsp.h — C-ABI of the B200 (sm_100a) active-vertex label-correcting sweep
+ * for the weight-constrained shortest path on subgraphs of Z^d (d = 1..4).
+ *
+ * The problem (§1): G(V, E) a subgraph of Z^d, f : E -> Z_+^2
+ * with f1(e) the passage time and f2(e) the weight of e; A, B disjoint vertex
+ * sets; a budget M.  Among all A->B paths pi with F2(pi) < M (strict,
+ * PAPER.md:21; reading R1 in DESIGN.md) find pi^ minimising F1(pi).  The
+ * output is F1(pi^) plus "the vertex X in B that is the endpoint of pi^, the
+ * last edge x on the path pi^, and the value F2(pi^)", with
+ * ties broken lexicographically on (F1, F2, X, Y), X and Y linear indices
+ * (reading R5).  The path itself is recovered by repeated solves on
+ * G'(V', E') (corrected as reading R12), see wcsp_reconstruct.
+ *
+ * The solve is the paper's per-unit-time cycle (§4, :155-227): water
+ * of quality M leaves A; every cycle advances the clock by the
+ * minimum live residual, counts down the active and phantom
+ * edges, triggers the destinations of the edges that reach 0, corrects labels
+ * (relabel + activate inactive vertices, phantom edges out of active ones,
+ * PAPER.md:32), retires vertices with no live edge, and stops at the first
+ * arrival at B (termination 1°) or when nothing is live (2°,
+ * PAPER.md:126).  Every step runs in the library's CUDA kernels; there is no
+ * CPU fallback (a missing or failing device returns WCSP_ECUDA).
+ *
+ * Encoding.  N = prod(shape) <= 2^30; vertex v = x0 + n0*(x1 + n1*(x2 + ...))
+ * (x0 fastest).  f1[k*N + v], f2[k*N + v] (uint8) are f1, f2 of the edge
+ * (v, v + e_k); f1 == 0 means "edge absent" (the subgraph of Z^d), values at
+ * x_k = n_k - 1 are ignored.  maskA, maskB: uint8 [N], nonzero = member.
+ * present: uint8 [N] or NULL; a vertex with present[v] == 0 is removed from
+ * G with all its edges (G' of PAPER.md:25).
+ *
+ * Ownership.  The caller owns every input array; inputs are read-only and may
+ * be freed once the call that takes them returns.  The handle owns all device
+ * state until wcsp_destroy.  `path`/`trace` outputs are caller-allocated.
+ *
+ * Errors.  Every call returns a wcsp_status; no exception crosses the ABI; on
+ * error the output structs are left untouched and wcsp_last_error() returns a
+ * thread-local message naming the offending input.
+ */
+#ifndef WCSP_H
+#define WCSP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  WCSP_REACHED = 0,     /* termination 1°: a vertex of B was reached */
+  WCSP_INFEASIBLE = 1,  /* termination 2°: no live edge left, no path with F2 < M */
+  WCSP_EINVAL = 2,      /* invalid input (validation rules below) */
+  WCSP_EMISMATCH = 3,   /* reconstruction: a re-solve on G' disagreed with the first solve */
+  WCSP_EBUDGET = 4,     /* options.cycle_budget exceeded */
+  WCSP_ENOMEM = 5,      /* device allocation failed */
+  WCSP_ECUDA = 6,       /* CUDA error (message in wcsp_last_error) */
+  WCSP_ENCCL = 7,       /* reserved: multi-GPU slab exchange */
+  WCSP_EOVERFLOW = 8    /* phantom pool overflow after the automatic retries */
+} wcsp_status;
+
+#define WCSP_M_INF (-1)           /* M = +infinity: first passage */
+#define WCSP_M_MAX 65533          /* largest finite M (16-bit labels) */
+
+enum { WCSP_MEM_HOST = 0, WCSP_MEM_DEVICE = 1 };
+enum { WCSP_JUMP = 0,             /* advance t by the min live residual */
+       WCSP_UNIT = 1 };           /* advance t by 1 — identical outputs */
+enum { WCSP_ENGINE_PERSISTENT = 0,/* one cooperative kernel runs every cycle (device-side termination) */
+       WCSP_ENGINE_STEPPED = 1 }; /* one kernel per phase, host polls termination every few cycles */
+
+/* Problem statement.  Validation (wcsp_create / wcsp_load):
+ *  d in 1..4, every shape[k] >= 1, N <= 2^30;  A and B non-empty among the
+ *  present vertices and disjoint;  M == WCSP_M_INF or
+ *  1 <= M <= WCSP_M_MAX;  every present edge (f1 > 0) has f2 >= 1
+ *  (f : E -> Z_+^2).  Violations return WCSP_EINVAL. */
+typedef struct {
+  int32_t d;
+  int64_t shape[4];
+  const uint8_t* f1;        /* [d][N] passage times, 0 = absent edge */
+  const uint8_t* f2;        /* [d][N] weights */
+  const uint8_t* maskA;     /* [N] sources: "vertices in A have label M" */
+  const uint8_t* maskB;     /* [N] targets */
+  const uint8_t* present;   /* [N] or NULL (all present) */
+  int64_t M;                /* budget, strict F2 < M, or WCSP_M_INF */
+  int32_t mem;              /* WCSP_MEM_HOST: host arrays (copied); WCSP_MEM_DEVICE: device
+                               pointers, read on options.stream during the call */
+} wcsp_problem;
+
+typedef struct {
+  int32_t time_mode;        /* WCSP_JUMP (default) | WCSP_UNIT */
+  int32_t engine;           /* WCSP_ENGINE_PERSISTENT (default) | WCSP_ENGINE_STEPPED */
+  int32_t demote_twin;      /* reserved (twin re-sourcing): must be 0 in this version */
+  int32_t device;           /* CUDA device ordinal */
+  int64_t cycle_budget;     /* 0 = unlimited; else WCSP_EBUDGET after that many cycles */
+  int64_t phantom_capacity; /* records per pool buffer; 0 = auto (4N, min 2^20); grown on overflow */
+  int64_t trace_cap;        /* per-cycle trace records kept (0 = off) */
+  void* stream;             /* cudaStream_t or NULL (the library creates one) */
+} wcsp_options;
+
+typedef struct {
+  int64_t F1;               /* t at termination 1° = F1(pi^) */
+  int64_t F2;               /* M - L(X); -1 when M = WCSP_M_INF */
+  int64_t X;                /* endpoint of pi^ in B (smallest index among ties) */
+  int64_t Y;                /* second-to-last vertex of pi^: the other endpoint of x, or the
+                               origin of the phantom that delivered it (the copy set C) */
+  int32_t x_lane;           /* lane of X toward Y: 2k = +e_k, 2k+1 = -e_k */
+  int32_t via_phantom;      /* 1 if the arrival at X was carried only by a phantom edge */
+  int64_t cycles;           /* cycles executed (time jumps) */
+  int64_t edge_updates;     /* sum over cycles of (live active edges + live phantom edges) */
+  int64_t arrivals;         /* edges/phantoms whose residual reached 0 */
+  int64_t triggered;        /* sum over cycles of triggered vertices */
+  int64_t phantoms_created;
+  int64_t relabels;
+  int64_t peak_active;      /* max active-vertex list size */
+  int64_t peak_phantoms;    /* max live phantoms */
+  int64_t phantom_capacity; /* pool capacity used by the successful run */
+  int64_t kernel_launches;  /* CUDA kernels this solve launched */
+  double device_ms;         /* device time of the solve (init + cycles), CUDA events */
+} wcsp_result;
+
+/* One record per cycle when options.trace_cap > 0 (after the cycle ran). */
+typedef struct {
+  int64_t t, delta;
+  int64_t active_vertices;  /* entries of the active-vertex list swept this cycle */
+  int64_t live_lanes;       /* E: live active edges at the top of the cycle */
+  int64_t phantoms;         /* P: live phantoms at the top of the cycle */
+  int64_t triggered;        /* T: vertices triggered this cycle */
+  int64_t arrivals;         /* R */
+  int64_t created;          /* phantoms created */
+  int64_t relabels;
+} wcsp_trace_rec;
+
+typedef struct wcsp_handle wcsp_handle;
+
+/* Allocate device state for the problem's shape and load it (validates). */
+wcsp_status wcsp_create(const wcsp_problem* problem, const wcsp_options* options, wcsp_handle** out);
+/* Re-load f1, f2, A, B, present, M into an existing handle of the same d/shape. */
+wcsp_status wcsp_load(wcsp_handle* h, const wcsp_problem* problem);
+/* Run the sweep on the loaded problem. Returns WCSP_REACHED / WCSP_INFEASIBLE or an error. */
+wcsp_status wcsp_solve(wcsp_handle* h, wcsp_result* result);
+/* Replace B (maskB != NULL), the present set (present != NULL; all present if
+ * present_all) and M for subsequent solves.  Arrays follow `mem`. */
+wcsp_status wcsp_set_targets(wcsp_handle* h, const uint8_t* maskB, const uint8_t* present,
+                             int32_t present_all, int64_t M, int32_t mem);
+/* Full path pi^ = (v_1 in A, ..., v_k = X in B) by repeated solves on G'
+ * (reading R12: B' = {Y}, V' = V \ (B u earlier targets),
+ * M' = F2 - f2(x) + 1).  Each re-solve must return (F1 - f1(x), F2 - f2(x)),
+ * else WCSP_EMISMATCH.  path has room for cap vertices; if cap is too small
+ * returns WCSP_EINVAL with *len = the required length.  Restores the loaded
+ * problem's B/present/M afterwards.  result = the first solve's result. */
+wcsp_status wcsp_reconstruct(wcsp_handle* h, int64_t* path, int64_t cap, int64_t* len, wcsp_result* result);
+/* Copy the last solve's trace (host memory). */
+wcsp_status wcsp_trace(wcsp_handle* h, wcsp_trace_rec* out, int64_t cap, int64_t* n);
+/* Host-side path check: path over present edges from A to B;
+ * writes F1, F2.  Returns 0 if valid with F2 < M, WCSP_INFEASIBLE if F2 >= M,
+ * WCSP_EINVAL otherwise.  Host arrays only. */
+wcsp_status wcsp_validate_path(const wcsp_problem* problem, const int64_t* path, int64_t len,
+                               int64_t* F1, int64_t* F2);
+void wcsp_destroy(wcsp_handle* h);
+const char* wcsp_last_error(void);
+/* Version string, and the number of SMs / cooperative blocks the persistent engine uses. */
+const char* wcsp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WCSP_H */

@@ -1,0 +1,596 @@
+// wcsp.cu — host side of the C-ABI (include/wcsp.h): handle, validation,
+// engines (persistent cooperative kernel / stepped kernels), reconstruction.
+#include "wcsp.h"
+#include "wcsp_device.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace wcspk;
+
+namespace {
+
+thread_local std::string g_err;
+
+wcsp_status fail(wcsp_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CK(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(e_ == cudaErrorMemoryAllocation ? WCSP_ENOMEM : WCSP_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
+  } while (0)
+
+}  // namespace
+
+struct wcsp_handle {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int d = 0;
+  long long shape[4] = {1, 1, 1, 1};
+  unsigned long long N = 0;
+  wcsp_options opt{};
+  // device buffers
+  uint8_t *d_f1 = nullptr, *d_f2 = nullptr;          // staging of host inputs [d][N]
+  uint8_t *d_maskA = nullptr, *d_maskB = nullptr, *d_present = nullptr;
+  uint8_t *d_maskB_saved = nullptr, *d_present_saved = nullptr;  // reconstruction
+  bool present_all = true, present_all_saved = true;
+  void* wt = nullptr;
+  void* res = nullptr;
+  unsigned short* label = nullptr;
+  unsigned long long* temp = nullptr;
+  unsigned* act[2] = {nullptr, nullptr};
+  unsigned* trig = nullptr;
+  unsigned long long* pool[2] = {nullptr, nullptr};
+  unsigned long long pool_cap = 0;
+  Ctl* ctl = nullptr;
+  Ctl* h_ctl = nullptr;                              // pinned
+  TraceRec* trace = nullptr;
+  unsigned long long* d_cnt = nullptr;               // validation counters
+  long long M = 0, M_saved = 0;
+  int nsm = 0, coop_blocks = 0, step_blocks = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  long long last_cycles = 0;
+  long long launches = 0;
+};
+
+namespace {
+
+size_t lane_bytes(int d) { return d <= 2 ? 4 : 8; }
+
+template <int D>
+void* persistent_fn() { return reinterpret_cast<void*>(&k_persistent<D>); }
+
+Dev make_dev(const wcsp_handle* h) {
+  Dev s{};
+  s.N = (unsigned)h->N;
+  s.NL = 2 * h->d;
+  unsigned long long st = 1;
+  for (int k = 0; k < 4; ++k) {
+    if (k < h->d) {
+      s.off[2 * k] = (unsigned)st;
+      s.off[2 * k + 1] = (unsigned)(0ull - st);
+      st *= (unsigned long long)h->shape[k];
+    } else {
+      s.off[2 * k] = s.off[2 * k + 1] = 0;
+    }
+  }
+  s.wt = h->wt;
+  s.res = h->res;
+  s.label = h->label;
+  s.temp = h->temp;
+  s.act[0] = h->act[0]; s.act[1] = h->act[1];
+  s.trig = h->trig;
+  s.pool[0] = h->pool[0]; s.pool[1] = h->pool[1];
+  s.pool_cap = h->pool_cap;
+  s.ctl = h->ctl;
+  s.trace = h->trace;
+  s.trace_cap = h->opt.trace_cap;
+  s.budget = h->opt.cycle_budget;
+  s.unit = h->opt.time_mode == WCSP_UNIT;
+  s.minf = h->M == WCSP_M_INF;
+  s.M = (int)(h->M == WCSP_M_INF ? 1 : h->M);
+  return s;
+}
+
+wcsp_status alloc_pool(wcsp_handle* h, unsigned long long cap) {
+  if (h->pool[0]) cudaFree(h->pool[0]);
+  if (h->pool[1]) cudaFree(h->pool[1]);
+  h->pool[0] = h->pool[1] = nullptr;
+  h->pool_cap = 0;
+  CK(cudaMalloc(&h->pool[0], cap * sizeof(unsigned long long)));
+  CK(cudaMalloc(&h->pool[1], cap * sizeof(unsigned long long)));
+  h->pool_cap = cap;
+  return WCSP_REACHED;
+}
+
+int grid_for(const wcsp_handle* h, unsigned long long n) {
+  unsigned long long b = (n + THREADS - 1) / THREADS;
+  return (int)std::max<unsigned long long>(1, std::min<unsigned long long>(b, (unsigned long long)h->nsm * 8));
+}
+
+wcsp_status check_M(long long M) {
+  if (M == WCSP_M_INF) return WCSP_REACHED;
+  if (M < 1 || M > WCSP_M_MAX)
+    return fail(WCSP_EINVAL, "M = %lld outside [1, %d] (and not WCSP_M_INF)", M, WCSP_M_MAX);
+  return WCSP_REACHED;
+}
+
+wcsp_status validate_device(wcsp_handle* h, const uint8_t* f1, const uint8_t* f2) {
+  CK(cudaMemsetAsync(h->d_cnt, 0, 4 * sizeof(unsigned long long), h->stream));
+  k_validate<<<grid_for(h, h->N), THREADS, 0, h->stream>>>(h->N, h->d, h->shape[0], h->shape[1], h->shape[2],
+                                                          h->shape[3], f1, f2, h->d_maskA, h->d_maskB,
+                                                          h->present_all ? nullptr : h->d_present, h->d_cnt);
+  CK(cudaGetLastError());
+  unsigned long long c[4];
+  CK(cudaMemcpyAsync(c, h->d_cnt, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (c[0] == 0) return fail(WCSP_EINVAL, "A is empty (among present vertices)");
+  if (c[1] == 0) return fail(WCSP_EINVAL, "B is empty (among present vertices)");
+  if (c[2] != 0) return fail(WCSP_EINVAL, "A and B intersect in %llu vertices", c[2]);
+  if (c[3] != 0) return fail(WCSP_EINVAL, "%llu present edges have f1 > 0 and f2 = 0", c[3]);
+  return WCSP_REACHED;
+}
+
+wcsp_status build_weights(wcsp_handle* h, const uint8_t* f1, const uint8_t* f2) {
+  Dev s = make_dev(h);
+  const int g = grid_for(h, h->N);
+  switch (h->d) {
+    case 1: k_weights<1><<<g, THREADS, 0, h->stream>>>(s, f1, f2, h->shape[0], 1, 1, 1); break;
+    case 2: k_weights<2><<<g, THREADS, 0, h->stream>>>(s, f1, f2, h->shape[0], h->shape[1], 1, 1); break;
+    case 3: k_weights<3><<<g, THREADS, 0, h->stream>>>(s, f1, f2, h->shape[0], h->shape[1], h->shape[2], 1); break;
+    default: k_weights<4><<<g, THREADS, 0, h->stream>>>(s, f1, f2, h->shape[0], h->shape[1], h->shape[2], h->shape[3]); break;
+  }
+  CK(cudaGetLastError());
+  return WCSP_REACHED;
+}
+
+wcsp_status copy_mask(wcsp_handle* h, uint8_t* dst, const uint8_t* src, int mem) {
+  CK(cudaMemcpyAsync(dst, src, h->N, mem == WCSP_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     h->stream));
+  return WCSP_REACHED;
+}
+
+wcsp_status load_problem(wcsp_handle* h, const wcsp_problem* p) {
+  wcsp_status st;
+  if ((st = check_M(p->M)) != WCSP_REACHED) return st;
+  if (!p->f1 || !p->f2 || !p->maskA || !p->maskB) return fail(WCSP_EINVAL, "f1, f2, maskA, maskB must be non-NULL");
+  const size_t fb = (size_t)h->d * h->N;
+  const uint8_t *f1 = p->f1, *f2 = p->f2;
+  if (p->mem == WCSP_MEM_HOST) {
+    CK(cudaMemcpyAsync(h->d_f1, p->f1, fb, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_f2, p->f2, fb, cudaMemcpyHostToDevice, h->stream));
+    f1 = h->d_f1;
+    f2 = h->d_f2;
+  } else if (p->mem != WCSP_MEM_DEVICE) {
+    return fail(WCSP_EINVAL, "mem must be WCSP_MEM_HOST or WCSP_MEM_DEVICE");
+  }
+  if ((st = copy_mask(h, h->d_maskA, p->maskA, p->mem)) != WCSP_REACHED) return st;
+  if ((st = copy_mask(h, h->d_maskB, p->maskB, p->mem)) != WCSP_REACHED) return st;
+  h->present_all = p->present == nullptr;
+  if (!h->present_all && (st = copy_mask(h, h->d_present, p->present, p->mem)) != WCSP_REACHED) return st;
+  if ((st = validate_device(h, f1, f2)) != WCSP_REACHED) return st;
+  if ((st = build_weights(h, f1, f2)) != WCSP_REACHED) return st;
+  h->M = p->M;
+  return WCSP_REACHED;
+}
+
+void release(wcsp_handle* h) {
+  void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->d_maskB_saved, h->d_present_saved,
+                  h->wt, h->res, h->label, h->temp, h->act[0], h->act[1], h->trig, h->pool[0], h->pool[1],
+                  h->ctl, h->trace, h->d_cnt};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (h->h_ctl) cudaFreeHost(h->h_ctl);
+  if (h->e0) cudaEventDestroy(h->e0);
+  if (h->e1) cudaEventDestroy(h->e1);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+}
+
+wcsp_status reset_ctl(wcsp_handle* h) {
+  Ctl c;
+  memset(&c, 0, sizeof(c));
+  c.view.t = 0;
+  c.view.c = 0;
+  c.view.stamp = stamp_of(0);
+  c.view.delta = 0;
+  c.view.cur = 0;
+  c.view.status = ST_RUNNING;
+  for (int i = 0; i < 3; ++i) c.acc[i].dmin = 0xFFFFFFFFu;
+  *h->h_ctl = c;
+  CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
+  return WCSP_REACHED;
+}
+
+wcsp_status launch_init(wcsp_handle* h) {
+  Dev s = make_dev(h);
+  k_init<<<grid_for(h, h->N), THREADS, 0, h->stream>>>(s, h->d_maskA, h->d_maskB,
+                                                      h->present_all ? nullptr : h->d_present,
+                                                      h->M == WCSP_M_INF ? 1 : (int)h->M, h->d);
+  CK(cudaGetLastError());
+  h->launches += 1;
+  return WCSP_REACHED;
+}
+
+wcsp_status run_persistent(wcsp_handle* h) {
+  Dev s = make_dev(h);
+  void* fn = nullptr;
+  switch (h->d) {
+    case 1: fn = persistent_fn<1>(); break;
+    case 2: fn = persistent_fn<2>(); break;
+    case 3: fn = persistent_fn<3>(); break;
+    default: fn = persistent_fn<4>(); break;
+  }
+  void* args[] = {&s};
+  CK(cudaLaunchCooperativeKernel(fn, dim3(h->coop_blocks), dim3(THREADS), args, 0, h->stream));
+  h->launches += 1;
+  return WCSP_REACHED;
+}
+
+template <int D>
+void launch_cycle(wcsp_handle* h, const Dev& s) {
+  k_sweep<D><<<h->step_blocks, THREADS, 0, h->stream>>>(s);
+  k_treat<D><<<h->step_blocks, THREADS, 0, h->stream>>>(s);
+  k_decide<<<1, 32, 0, h->stream>>>(s);
+}
+
+wcsp_status run_stepped(wcsp_handle* h) {
+  Dev s = make_dev(h);
+  int batch = 4;
+  for (;;) {
+    for (int i = 0; i < batch; ++i) {
+      switch (h->d) {
+        case 1: launch_cycle<1>(h, s); break;
+        case 2: launch_cycle<2>(h, s); break;
+        case 3: launch_cycle<3>(h, s); break;
+        default: launch_cycle<4>(h, s); break;
+      }
+      h->launches += 3;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&h->h_ctl->view, &h->ctl->view, sizeof(View), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const int st = h->h_ctl->view.status;
+    if (st == ST_WRAP) {
+      CK(cudaMemsetAsync(h->temp, 0, h->N * sizeof(unsigned long long), h->stream));
+      const int run = ST_RUNNING;
+      CK(cudaMemcpyAsync(&h->ctl->view.status, &run, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      continue;
+    }
+    if (st != ST_RUNNING) break;
+    batch = std::min(batch * 2, 64);
+  }
+  return WCSP_REACHED;
+}
+
+int x_lane_of(const wcsp_handle* h, long long X, long long Y) {
+  long long st = 1;
+  for (int k = 0; k < h->d; ++k) {
+    if (Y == X + st) return 2 * k;
+    if (Y == X - st) return 2 * k + 1;
+    st *= h->shape[k];
+  }
+  return -1;
+}
+
+wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
+  wcsp_status st;
+  h->launches = 0;
+  CK(cudaEventRecord(h->e0, h->stream));
+  if ((st = reset_ctl(h)) != WCSP_REACHED) return st;
+  if ((st = launch_init(h)) != WCSP_REACHED) return st;
+  if (h->opt.engine == WCSP_ENGINE_STEPPED)
+    st = run_stepped(h);
+  else
+    st = run_persistent(h);
+  if (st != WCSP_REACHED) return st;
+  CK(cudaEventRecord(h->e1, h->stream));
+  CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, h->e0, h->e1));
+  const Ctl& c = *h->h_ctl;
+  *status = c.view.status;
+  memset(r, 0, sizeof(*r));
+  r->F1 = c.F1;
+  r->F2 = c.F2;
+  r->X = c.X;
+  r->Y = c.Y;
+  r->via_phantom = (int)c.via;
+  r->x_lane = *status == WCSP_REACHED ? x_lane_of(h, c.X, c.Y) : -1;
+  if (*status != WCSP_REACHED) r->F1 = r->F2 = r->X = r->Y = -1;
+  r->cycles = c.cycles;
+  r->edge_updates = c.edge_updates;
+  r->arrivals = c.arrivals;
+  r->triggered = c.triggered;
+  r->phantoms_created = c.created;
+  r->relabels = c.relabels;
+  r->peak_active = c.peak_active;
+  r->peak_phantoms = c.peak_phantoms;
+  r->phantom_capacity = (long long)h->pool_cap;
+  r->kernel_launches = h->launches;
+  r->device_ms = ms;
+  h->last_cycles = c.cycles;
+  if (*status == WCSP_EOVERFLOW) r->phantom_capacity = c.need_pool;
+  return WCSP_REACHED;
+}
+
+wcsp_status solve_impl(wcsp_handle* h, wcsp_result* out) {
+  wcsp_result r;
+  int status = ST_RUNNING;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    wcsp_status st = solve_once(h, &r, &status);
+    if (st != WCSP_REACHED) return st;
+    if (status != WCSP_EOVERFLOW) break;
+    // phantom pool overflow: grow to the observed need and re-run (device flag -> host retry)
+    const unsigned long long need = (unsigned long long)r.phantom_capacity;
+    const unsigned long long cap = std::max(need + need / 2, h->pool_cap * 2);
+    if ((st = alloc_pool(h, cap)) != WCSP_REACHED) return st;
+  }
+  if (status == WCSP_EOVERFLOW) return fail(WCSP_EOVERFLOW, "phantom pool overflow (need %lld)", r.phantom_capacity);
+  if (status == WCSP_EBUDGET) { *out = r; return fail(WCSP_EBUDGET, "cycle budget %lld exceeded", h->opt.cycle_budget); }
+  if (status != WCSP_REACHED && status != WCSP_INFEASIBLE) return fail(WCSP_ECUDA, "solver ended in state %d", status);
+  *out = r;
+  return (wcsp_status)status;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wcsp_last_error(void) { return g_err.c_str(); }
+
+const char* wcsp_version(void) { return "wcsp-b200 0.1 (sm_100a; persistent + stepped engines)"; }
+
+wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handle** out) {
+  if (!p || !out) return fail(WCSP_EINVAL, "problem and out must be non-NULL");
+  if (p->d < 1 || p->d > 4) return fail(WCSP_EINVAL, "d = %d outside 1..4", p->d);
+  unsigned long long N = 1;
+  for (int k = 0; k < p->d; ++k) {
+    if (p->shape[k] < 1) return fail(WCSP_EINVAL, "shape[%d] = %lld < 1", k, (long long)p->shape[k]);
+    N *= (unsigned long long)p->shape[k];
+    if (N > (1ull << 30)) return fail(WCSP_EINVAL, "N > 2^30 vertices");
+  }
+  wcsp_status st;
+  if ((st = check_M(p->M)) != WCSP_REACHED) return st;
+  wcsp_options opt{};
+  if (o) opt = *o;
+  if (opt.demote_twin) return fail(WCSP_EINVAL, "demote_twin is reserved in this version (must be 0)");
+  if (opt.time_mode != WCSP_JUMP && opt.time_mode != WCSP_UNIT) return fail(WCSP_EINVAL, "bad time_mode");
+  if (opt.engine != WCSP_ENGINE_PERSISTENT && opt.engine != WCSP_ENGINE_STEPPED) return fail(WCSP_EINVAL, "bad engine");
+  if (opt.trace_cap < 0 || opt.cycle_budget < 0 || opt.phantom_capacity < 0) return fail(WCSP_EINVAL, "negative option");
+
+  wcsp_handle* h = new wcsp_handle();
+  h->opt = opt;
+  h->d = p->d;
+  for (int k = 0; k < 4; ++k) h->shape[k] = k < p->d ? p->shape[k] : 1;
+  h->N = N;
+  h->dev = opt.device;
+#define CKH(call)                       \
+  do {                                  \
+    wcsp_status s_ = (call);            \
+    if (s_ != WCSP_REACHED) {           \
+      release(h);                       \
+      delete h;                         \
+      return s_;                        \
+    }                                   \
+  } while (0)
+#define CKC(call) CKH([&]() -> wcsp_status { CK(call); return WCSP_REACHED; }())
+  CKC(cudaSetDevice(h->dev));
+  if (opt.stream) {
+    h->stream = (cudaStream_t)opt.stream;
+  } else {
+    CKC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  CKC(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  int per_sm = 0;
+  void* fn = p->d == 1 ? persistent_fn<1>() : p->d == 2 ? persistent_fn<2>() : p->d == 3 ? persistent_fn<3>() : persistent_fn<4>();
+  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, 0));
+  if (per_sm < 1) CKH(fail(WCSP_ECUDA, "persistent kernel cannot be resident"));
+  h->coop_blocks = per_sm * h->nsm;
+  h->step_blocks = per_sm * h->nsm;
+  const size_t fb = (size_t)h->d * N;
+  CKC(cudaMalloc(&h->d_f1, fb));
+  CKC(cudaMalloc(&h->d_f2, fb));
+  CKC(cudaMalloc(&h->d_maskA, N));
+  CKC(cudaMalloc(&h->d_maskB, N));
+  CKC(cudaMalloc(&h->d_present, N));
+  CKC(cudaMalloc(&h->wt, N * 2 * lane_bytes(h->d)));
+  CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
+  CKC(cudaMalloc(&h->label, N * sizeof(unsigned short)));
+  CKC(cudaMalloc(&h->temp, N * sizeof(unsigned long long)));
+  CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));
+  CKC(cudaMalloc(&h->act[1], N * sizeof(unsigned)));
+  CKC(cudaMalloc(&h->trig, N * sizeof(unsigned)));
+  CKC(cudaMalloc(&h->ctl, sizeof(Ctl)));
+  CKC(cudaMallocHost(&h->h_ctl, sizeof(Ctl)));
+  CKC(cudaMalloc(&h->d_cnt, 4 * sizeof(unsigned long long)));
+  CKC(cudaMalloc(&h->trace, std::max<long long>(1, opt.trace_cap) * sizeof(TraceRec)));
+  CKC(cudaEventCreate(&h->e0));
+  CKC(cudaEventCreate(&h->e1));
+  const unsigned long long cap = opt.phantom_capacity > 0 ? (unsigned long long)opt.phantom_capacity
+                                                          : std::max<unsigned long long>(4 * N, 1ull << 20);
+  CKH(alloc_pool(h, cap));
+  CKH(load_problem(h, p));
+#undef CKC
+#undef CKH
+  *out = h;
+  return WCSP_REACHED;
+}
+
+wcsp_status wcsp_load(wcsp_handle* h, const wcsp_problem* p) {
+  if (!h || !p) return fail(WCSP_EINVAL, "NULL argument");
+  if (p->d != h->d) return fail(WCSP_EINVAL, "d differs from the handle's");
+  for (int k = 0; k < h->d; ++k)
+    if (p->shape[k] != h->shape[k]) return fail(WCSP_EINVAL, "shape differs from the handle's");
+  CK(cudaSetDevice(h->dev));
+  return load_problem(h, p);
+}
+
+wcsp_status wcsp_solve(wcsp_handle* h, wcsp_result* r) {
+  if (!h || !r) return fail(WCSP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(h->dev));
+  return solve_impl(h, r);
+}
+
+wcsp_status wcsp_set_targets(wcsp_handle* h, const uint8_t* maskB, const uint8_t* present, int32_t present_all,
+                             int64_t M, int32_t mem) {
+  if (!h) return fail(WCSP_EINVAL, "NULL handle");
+  wcsp_status st;
+  if ((st = check_M(M)) != WCSP_REACHED) return st;
+  CK(cudaSetDevice(h->dev));
+  if (maskB && (st = copy_mask(h, h->d_maskB, maskB, mem)) != WCSP_REACHED) return st;
+  if (present_all) h->present_all = true;
+  else if (present) {
+    if ((st = copy_mask(h, h->d_present, present, mem)) != WCSP_REACHED) return st;
+    h->present_all = false;
+  }
+  h->M = M;
+  CK(cudaStreamSynchronize(h->stream));
+  return WCSP_REACHED;
+}
+
+wcsp_status wcsp_trace(wcsp_handle* h, wcsp_trace_rec* out, int64_t cap, int64_t* n) {
+  if (!h || !n) return fail(WCSP_EINVAL, "NULL argument");
+  const long long avail = std::min<long long>(h->last_cycles, h->opt.trace_cap);
+  const long long m = std::min<long long>(avail, cap);
+  static_assert(sizeof(TraceRec) == sizeof(wcsp_trace_rec), "trace record layout");
+  if (m > 0) {
+    CK(cudaMemcpyAsync(out, h->trace, m * sizeof(TraceRec), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  *n = m;
+  return WCSP_REACHED;
+}
+
+// Reconstruction (reading R12 in DESIGN.md).
+wcsp_status wcsp_reconstruct(wcsp_handle* h, int64_t* path, int64_t cap, int64_t* len, wcsp_result* result) {
+  if (!h || !len) return fail(WCSP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(h->dev));
+  const unsigned long long N = h->N;
+  wcsp_result first;
+  wcsp_status st = solve_impl(h, &first);
+  if (st != WCSP_REACHED) return st;
+  // host views of what the driver needs: A, B, present, and the edge values at each step
+  std::vector<uint8_t> A(N), B(N), pres(N, 1);
+  CK(cudaMemcpyAsync(A.data(), h->d_maskA, N, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(B.data(), h->d_maskB, N, cudaMemcpyDeviceToHost, h->stream));
+  if (!h->present_all) CK(cudaMemcpyAsync(pres.data(), h->d_present, N, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  const bool saved_all = h->present_all;
+  const long long saved_M = h->M;
+  std::vector<uint8_t> pres0 = pres;
+  std::vector<int64_t> rev;   // X, then predecessors
+  rev.push_back(first.X);
+  long long X = first.X, Y = first.Y, F1 = first.F1, F2 = first.F2;
+  // V' = V \ B: remove every target
+  std::vector<uint8_t> work = pres;
+  for (unsigned long long v = 0; v < N; ++v)
+    if (B[v]) work[v] = 0;
+  std::vector<uint8_t> onlyY(N, 0);
+  auto edge_f = [&](long long u, long long v, int* f1, int* f2) -> wcsp_status {
+    // weight record of u, lane toward v
+    const int lane = x_lane_of(h, u, v);
+    if (lane < 0) return fail(WCSP_EMISMATCH, "reconstruction: %lld and %lld are not lattice neighbours", u, v);
+    const size_t lb = lane_bytes(h->d);
+    unsigned char rec[16];
+    CK(cudaMemcpy(rec, (const char*)h->wt + (size_t)u * 2 * lb, 2 * lb, cudaMemcpyDeviceToHost));
+    *f1 = rec[lane];
+    *f2 = rec[lb + lane];
+    return WCSP_REACHED;
+  };
+  wcsp_status out = WCSP_REACHED;
+  while (!A[(size_t)Y]) {
+    if ((long long)rev.size() > (long long)N) { out = fail(WCSP_EMISMATCH, "reconstruction does not terminate"); break; }
+    int f1x = 0, f2x = 0;
+    if ((out = edge_f(Y, X, &f1x, &f2x)) != WCSP_REACHED) break;
+    // B' = {Y}, M' = F2 - f2(x) + 1 (reading R12), V' = V \ (B u earlier targets)
+    std::fill(onlyY.begin(), onlyY.end(), 0);
+    onlyY[(size_t)Y] = 1;
+    const long long Mp = h->M == WCSP_M_INF ? WCSP_M_INF : F2 - f2x + 1;
+    CK(cudaMemcpyAsync(h->d_maskB, onlyY.data(), N, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_present, work.data(), N, cudaMemcpyHostToDevice, h->stream));
+    h->present_all = false;
+    h->M = Mp;
+    wcsp_result r;
+    st = solve_impl(h, &r);
+    h->M = saved_M;
+    if (st != WCSP_REACHED) { out = fail(WCSP_EMISMATCH, "re-solve toward %lld returned status %d", Y, (int)st); break; }
+    const long long want1 = F1 - f1x, want2 = saved_M == WCSP_M_INF ? -1 : F2 - f2x;
+    if (r.F1 != want1 || r.F2 != want2 || r.X != Y) {
+      out = fail(WCSP_EMISMATCH, "re-solve toward %lld gave (F1, F2) = (%lld, %lld), expected (%lld, %lld)", Y,
+                 (long long)r.F1, (long long)r.F2, want1, want2);
+      break;
+    }
+    rev.push_back(Y);
+    work[(size_t)Y] = 0;
+    X = Y; Y = r.Y; F1 = r.F1; F2 = r.F2;
+    if (saved_M == WCSP_M_INF) F2 = -1;
+  }
+  if (out == WCSP_REACHED) rev.push_back(Y);
+  // restore the loaded problem
+  CK(cudaMemcpyAsync(h->d_maskB, B.data(), N, cudaMemcpyHostToDevice, h->stream));
+  if (!saved_all) CK(cudaMemcpyAsync(h->d_present, pres0.data(), N, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->present_all = saved_all;
+  h->M = saved_M;
+  if (out != WCSP_REACHED) return out;
+  *len = (int64_t)rev.size();
+  if (result) *result = first;
+  if (!path || cap < (int64_t)rev.size()) return fail(WCSP_EINVAL, "path capacity %lld < %lld", (long long)cap, (long long)rev.size());
+  for (size_t i = 0; i < rev.size(); ++i) path[i] = rev[rev.size() - 1 - i];
+  return WCSP_REACHED;
+}
+
+wcsp_status wcsp_validate_path(const wcsp_problem* p, const int64_t* path, int64_t len, int64_t* F1, int64_t* F2) {
+  if (!p || !path || len < 2 || p->mem != WCSP_MEM_HOST) return fail(WCSP_EINVAL, "bad arguments");
+  long long N = 1, st[4] = {1, 1, 1, 1};
+  for (int k = 0; k < p->d; ++k) { st[k] = N; N *= p->shape[k]; }
+  auto present = [&](long long v) { return p->present == nullptr || p->present[v] != 0; };
+  for (int64_t i = 0; i < len; ++i)
+    if (path[i] < 0 || path[i] >= N || !present(path[i])) return fail(WCSP_EINVAL, "path[%lld] invalid", (long long)i);
+  if (!p->maskA[path[0]]) return fail(WCSP_EINVAL, "path does not start in A");
+  if (!p->maskB[path[len - 1]]) return fail(WCSP_EINVAL, "path does not end in B");
+  long long s1 = 0, s2 = 0;
+  for (int64_t i = 0; i + 1 < len; ++i) {
+    const long long u = std::min(path[i], path[i + 1]), v = std::max(path[i], path[i + 1]);
+    int k = -1;
+    for (int j = 0; j < p->d; ++j)
+      if (v - u == st[j] && (u / st[j]) % p->shape[j] + 1 < p->shape[j]) k = j;
+    if (k < 0 || p->f1[(size_t)k * N + u] == 0) return fail(WCSP_EINVAL, "no edge between path[%lld] and path[%lld]", (long long)i, (long long)i + 1);
+    s1 += p->f1[(size_t)k * N + u];
+    s2 += p->f2[(size_t)k * N + u];
+  }
+  *F1 = s1;
+  *F2 = s2;
+  if (p->M != WCSP_M_INF && s2 >= p->M) return WCSP_INFEASIBLE;
+  return WCSP_REACHED;
+}
+
+void wcsp_destroy(wcsp_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  release(h);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,289 @@
+"""Thin Python binding of the C-ABI in include/wcsp.h (argument marshalling only).
+
+Every step of the solve runs in libwcsp.so's CUDA kernels; this module only
+packs pointers and sizes.  There is no CPU fallback: if libwcsp.so is missing
+or no CUDA device is usable the calls raise.
+
+Inputs are either an `instances.Instance` (host numpy arrays -> WCSP_MEM_HOST)
+or torch CUDA tensors (WCSP_MEM_DEVICE, read on the solver's stream).
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+from typing import Optional
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libwcsp.so")
+
+M_INF = -1
+M_MAX = 65533
+REACHED, INFEASIBLE, EINVAL, EMISMATCH, EBUDGET, ENOMEM, ECUDA, ENCCL, EOVERFLOW = range(9)
+MEM_HOST, MEM_DEVICE = 0, 1
+JUMP, UNIT = 0, 1
+PERSISTENT, STEPPED = 0, 1
+_STATUS = {0: "REACHED", 1: "INFEASIBLE", 2: "EINVAL", 3: "EMISMATCH", 4: "EBUDGET", 5: "ENOMEM",
+           6: "ECUDA", 7: "ENCCL", 8: "EOVERFLOW"}
+
+
+class WcspError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"wcsp {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("shape", ctypes.c_int64 * 4),
+                ("f1", ctypes.c_void_p), ("f2", ctypes.c_void_p),
+                ("maskA", ctypes.c_void_p), ("maskB", ctypes.c_void_p), ("present", ctypes.c_void_p),
+                ("M", ctypes.c_int64), ("mem", ctypes.c_int32)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("time_mode", ctypes.c_int32), ("engine", ctypes.c_int32), ("demote_twin", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("cycle_budget", ctypes.c_int64),
+                ("phantom_capacity", ctypes.c_int64), ("trace_cap", ctypes.c_int64),
+                ("stream", ctypes.c_void_p)]
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [("F1", ctypes.c_int64), ("F2", ctypes.c_int64), ("X", ctypes.c_int64), ("Y", ctypes.c_int64),
+                ("x_lane", ctypes.c_int32), ("via_phantom", ctypes.c_int32),
+                ("cycles", ctypes.c_int64), ("edge_updates", ctypes.c_int64), ("arrivals", ctypes.c_int64),
+                ("triggered", ctypes.c_int64), ("phantoms_created", ctypes.c_int64),
+                ("relabels", ctypes.c_int64), ("peak_active", ctypes.c_int64),
+                ("peak_phantoms", ctypes.c_int64), ("phantom_capacity", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64), ("device_ms", ctypes.c_double)]
+
+
+TRACE_FIELDS = ["t", "delta", "active_vertices", "live_lanes", "phantoms", "triggered", "arrivals",
+                "created", "relabels"]
+
+
+class _TraceRec(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in TRACE_FIELDS]
+
+
+EXPORTS = ["wcsp_create", "wcsp_load", "wcsp_solve", "wcsp_set_targets", "wcsp_reconstruct", "wcsp_trace",
+           "wcsp_validate_path", "wcsp_destroy", "wcsp_last_error", "wcsp_version"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libwcsp.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with `python -m paper_1511_06441_b200.build` "
+                           "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, O, R = ctypes.POINTER(_Problem), ctypes.POINTER(_Options), ctypes.POINTER(_Result)
+    lib.wcsp_create.argtypes = [P, O, ctypes.POINTER(ctypes.c_void_p)]
+    lib.wcsp_load.argtypes = [ctypes.c_void_p, P]
+    lib.wcsp_solve.argtypes = [ctypes.c_void_p, R]
+    lib.wcsp_set_targets.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                     ctypes.c_int64, ctypes.c_int32]
+    lib.wcsp_reconstruct.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+                                     ctypes.POINTER(ctypes.c_int64), R]
+    lib.wcsp_trace.argtypes = [ctypes.c_void_p, ctypes.POINTER(_TraceRec), ctypes.c_int64,
+                               ctypes.POINTER(ctypes.c_int64)]
+    lib.wcsp_validate_path.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+                                       ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    for f in ("wcsp_create", "wcsp_load", "wcsp_solve", "wcsp_set_targets", "wcsp_reconstruct", "wcsp_trace",
+              "wcsp_validate_path"):
+        getattr(lib, f).restype = ctypes.c_int
+    lib.wcsp_destroy.argtypes = [ctypes.c_void_p]
+    lib.wcsp_destroy.restype = None
+    lib.wcsp_last_error.restype = ctypes.c_char_p
+    lib.wcsp_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load_library().wcsp_last_error().decode()
+
+
+@dataclasses.dataclass
+class Result:
+    status: int
+    F1: int = -1
+    F2: int = -1
+    X: int = -1
+    Y: int = -1
+    x_lane: int = -1
+    via_phantom: int = 0
+    cycles: int = 0
+    edge_updates: int = 0
+    arrivals: int = 0
+    triggered: int = 0
+    phantoms_created: int = 0
+    relabels: int = 0
+    peak_active: int = 0
+    peak_phantoms: int = 0
+    phantom_capacity: int = 0
+    kernel_launches: int = 0
+    device_ms: float = 0.0
+
+    def key(self):
+        """Outputs compared bit-exactly with the oracle: (status, F1, F2, X, Y)."""
+        if self.status != REACHED:
+            return (self.status,)
+        return (self.status, self.F1, self.F2, self.X, self.Y)
+
+
+def _res(st: int, r: _Result) -> Result:
+    out = Result(st)
+    for f, _ in _Result._fields_:
+        setattr(out, f, getattr(r, f))
+    return out
+
+
+def _ptr(a, keep):
+    """(pointer, mem) of a host numpy array or a torch CUDA tensor (uint8)."""
+    if a is None:
+        return None, None
+    if hasattr(a, "data_ptr") and getattr(a, "is_cuda", False):
+        assert a.is_contiguous() and a.element_size() == 1
+        keep.append(a)
+        return a.data_ptr(), MEM_DEVICE
+    arr = np.ascontiguousarray(np.asarray(a), dtype=np.uint8)
+    keep.append(arr)
+    return arr.ctypes.data, MEM_HOST
+
+
+def _problem(shape, f1, f2, maskA, maskB, present, M):
+    keep = []
+    p = _Problem()
+    p.d = len(shape)
+    for k in range(4):
+        p.shape[k] = int(shape[k]) if k < len(shape) else 1
+    mems = set()
+    for name, a in (("f1", f1), ("f2", f2), ("maskA", maskA), ("maskB", maskB), ("present", present)):
+        ptr, mem = _ptr(a, keep)
+        setattr(p, name, ptr)
+        if mem is not None:
+            mems.add(mem)
+    if len(mems) != 1:
+        raise ValueError("inputs must be all host arrays or all CUDA tensors")
+    p.mem = mems.pop()
+    p.M = int(M)
+    return p, keep
+
+
+class Solver:
+    """A problem resident on one B200; `solve()` runs the sweep."""
+
+    def __init__(self, inst=None, *, shape=None, f1=None, f2=None, maskA=None, maskB=None, present=None,
+                 M=None, time_mode: str = "jump", engine: str = "persistent", trace_cap: int = 0,
+                 phantom_capacity: int = 0, cycle_budget: int = 0, device: int = 0, stream=None):
+        lib = load_library()
+        self._lib = lib
+        self._h = ctypes.c_void_p()
+        if inst is not None:
+            shape, f1, f2, maskA, maskB, present, M = (inst.shape, inst.f1, inst.f2, inst.maskA, inst.maskB,
+                                                       inst.present, inst.M)
+        self.shape = tuple(shape)
+        self.N = int(np.prod(self.shape))
+        o = _Options()
+        o.time_mode = {"jump": JUMP, "unit": UNIT}[time_mode]
+        o.engine = {"persistent": PERSISTENT, "stepped": STEPPED}[engine]
+        o.demote_twin = 0
+        o.device = int(device)
+        o.cycle_budget = int(cycle_budget)
+        o.phantom_capacity = int(phantom_capacity)
+        o.trace_cap = int(trace_cap)
+        o.stream = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        self.trace_cap = int(trace_cap)
+        p, keep = _problem(self.shape, f1, f2, maskA, maskB, present, M)
+        st = lib.wcsp_create(ctypes.byref(p), ctypes.byref(o), ctypes.byref(self._h))
+        if st != REACHED:
+            self._h = None
+            raise WcspError(st, last_error())
+
+    def load(self, inst=None, *, f1=None, f2=None, maskA=None, maskB=None, present=None, M=None):
+        if inst is not None:
+            f1, f2, maskA, maskB, present, M = inst.f1, inst.f2, inst.maskA, inst.maskB, inst.present, inst.M
+        p, keep = _problem(self.shape, f1, f2, maskA, maskB, present, M)
+        st = self._lib.wcsp_load(self._h, ctypes.byref(p))
+        if st != REACHED:
+            raise WcspError(st, last_error())
+
+    def solve(self) -> Result:
+        r = _Result()
+        st = self._lib.wcsp_solve(self._h, ctypes.byref(r))
+        if st not in (REACHED, INFEASIBLE):
+            raise WcspError(st, last_error())
+        return _res(st, r)
+
+    def set_targets(self, maskB=None, present=None, present_all: bool = False, M: int = None):
+        keep = []
+        pb, mb = _ptr(maskB, keep)
+        pp, mp = _ptr(present, keep)
+        mem = mb if mb is not None else (mp if mp is not None else MEM_HOST)
+        st = self._lib.wcsp_set_targets(self._h, pb, pp, int(present_all), int(M), mem)
+        if st != REACHED:
+            raise WcspError(st, last_error())
+
+    def reconstruct(self, cap: Optional[int] = None):
+        """(path list A -> ... -> X, Result of the first solve)."""
+        cap = cap or self.N
+        buf = (ctypes.c_int64 * cap)()
+        n = ctypes.c_int64(0)
+        r = _Result()
+        st = self._lib.wcsp_reconstruct(self._h, buf, cap, ctypes.byref(n), ctypes.byref(r))
+        if st != REACHED:
+            raise WcspError(st, last_error())
+        return [int(buf[i]) for i in range(n.value)], _res(st, r)
+
+    def trace(self) -> dict:
+        """Per-cycle counters of the last solve: dict of numpy int64 arrays."""
+        cap = max(1, self.trace_cap)
+        buf = (_TraceRec * cap)()
+        n = ctypes.c_int64(0)
+        st = self._lib.wcsp_trace(self._h, buf, cap, ctypes.byref(n))
+        if st != REACHED:
+            raise WcspError(st, last_error())
+        arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_int64)), shape=(cap, 9))[: n.value]
+        return {f: arr[:, i].copy() for i, f in enumerate(TRACE_FIELDS)}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wcsp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def solve(inst, **kw) -> Result:
+    with Solver(inst, **kw) as s:
+        return s.solve()
+
+
+def validate_path(inst, path):
+    """Host-side check through the C-ABI: (status, F1, F2)."""
+    lib = load_library()
+    p, keep = _problem(inst.shape, inst.f1, inst.f2, inst.maskA, inst.maskB, inst.present, inst.M)
+    arr = (ctypes.c_int64 * len(path))(*[int(x) for x in path])
+    f1, f2 = ctypes.c_int64(0), ctypes.c_int64(0)
+    st = lib.wcsp_validate_path(ctypes.byref(p), arr, len(path), ctypes.byref(f1), ctypes.byref(f2))
+    return int(st), int(f1.value), int(f2.value)
+
+
+def version() -> str:
+    return load_library().wcsp_version().decode()

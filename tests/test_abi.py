@@ -1,0 +1,71 @@
+"""C-ABI library checks that need no GPU (-m "not gpu"): the library builds and
+loads, exports every symbol include/wcsp.h declares, its host-only entry point
+(wcsp_validate_path) agrees with the oracle, and the compute entry points fail
+loudly instead of falling back to the CPU when no device is usable."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1511_06441_b200 import build, instances as I, wcsp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "wcsp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(wcsp_[a-z_]+)\s*\(", src)))
+
+
+def test_library_builds_and_exports_every_declared_symbol():
+    build.build()
+    lib = wcsp.load_library()
+    names = header_functions()
+    assert set(names) == set(wcsp.EXPORTS), names
+    for n in names:
+        assert hasattr(lib, n), n
+    # the exported dynamic symbols really are plain C names
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", wcsp.LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}$", out, flags=re.M), n
+
+
+def test_kernels_are_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", wcsp.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_validate_path_host_side_matches_oracle():
+    rng = np.random.default_rng(3)
+    for _ in range(30):
+        inst = I.random_small(rng, shapes=[(5, 5), (4, 3, 2)], M_range=(5, 40))
+        # a random walk from A that stops at the first B vertex (or after 12 steps)
+        v = int(np.flatnonzero(inst.maskA)[0])
+        path = [v]
+        for _ in range(12):
+            nb = [u for u in range(inst.N) if oracle.validate_path(inst.with_sets(
+                maskA=np.eye(1, inst.N, v, dtype=np.uint8)[0], maskB=np.eye(1, inst.N, u, dtype=np.uint8)[0]),
+                [v, u])[0] in (0, oracle.INFEASIBLE)]
+            if not nb:
+                break
+            v = int(rng.choice(nb))
+            path.append(v)
+        got = wcsp.validate_path(inst, path)
+        want = oracle.validate_path(inst, path)
+        assert got[0] == want[0]
+        if got[0] in (0, 1):
+            assert got[1:] == want[1:]
+
+
+def test_compute_entry_points_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(wcsp.WcspError) as e:
+        wcsp.solve(I.fixture_B())
+    assert e.value.status == wcsp.ECUDA

@@ -1,0 +1,195 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle (-m gpu).
+
+Bar: integer outputs (status, F1, F2, X, Y) bit-exact;
+with the default options (no twin demotion) the work counters
+(cycles, edge_updates = sum over cycles of live edges + phantoms) also equal
+the oracle's tier-2 counters exactly (same label semantics, DESIGN.md R-notes).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1511_06441_b200 import instances as I
+from paper_1511_06441_b200 import wcsp
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fixtures.json")))
+ENGINES = ["persistent", "stepped"]
+
+
+def check(inst, engine="persistent", time_mode="jump", counters=True, want=None):
+    r = wcsp.solve(inst, engine=engine, time_mode=time_mode)
+    o = oracle.solve_pruned(inst)
+    assert r.key() == o.key(), (inst.name, inst.seed, inst.shape, inst.M, r, o)
+    if want is not None:
+        assert r.key() == want.key()
+    if counters and time_mode == "jump":
+        assert (r.cycles, r.edge_updates) == (o.cycles, o.work), (inst.name, r, o)
+    return r, o
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("name", ["fixtureB", "fixtureD"])
+def test_mechanism_fixtures(name, engine):
+    inst = getattr(I, "fixture_" + name[-1])()
+    e = GOLD[name]["expect"]
+    with wcsp.Solver(inst, engine=engine, trace_cap=64) as s:
+        r = s.solve()
+        tr = s.trace()
+    assert r.key() == (wcsp.REACHED, e["F1"], e["F2"], e["X"], e["Y"])
+    # the narrated events: a phantom is created exactly at t = 13 (PAPER.md:85 / :97)
+    ev = [x for x in GOLD[name]["events"] if "phantom_label" in x][0]
+    t_created = tr["t"][tr["created"] > 0]
+    assert list(t_created) == [ev["t"]]
+    assert r.phantoms_created == 1
+    # every narrated relabel time is a cycle of the run (jump mode visits exactly these times)
+    for x in GOLD[name]["events"]:
+        assert x["t"] in set(tr["t"].tolist())
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_random_tiny_vs_brute_force(engine):
+    rng = np.random.default_rng(101)
+    shapes = [(3, 3), (4, 4), (5, 4), (2, 2, 2), (3, 2, 2), (6, 3), (7,)]
+    for i in range(150):
+        inst = I.random_small(rng, shapes=shapes, M_range=(3, 25), max_sources=2, max_targets=2,
+                              hole_prob=0.15 if i % 3 == 0 else 0.0)
+        if i % 10 == 9:
+            inst = inst.with_M(I.M_INF)
+        r, _ = check(inst, engine)
+        assert r.key() == oracle.solve_brute(inst).key()
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_random_mid_sizes(engine):
+    rng = np.random.default_rng(202 if engine == "persistent" else 203)
+    shapes = [(8, 8), (12, 12), (16, 16), (33, 7), (4, 4, 4), (6, 5, 4), (40,), (3, 3, 3, 3), (40, 40), (10, 10, 10)]
+    n_inf = 0
+    for i in range(300):
+        inst = I.random_small(rng, shapes=shapes, M_range=(5, 120), max_sources=4, max_targets=4,
+                              hole_prob=0.1 if i % 4 == 0 else 0.0)
+        r, _ = check(inst, engine)
+        if inst.M * inst.N <= 2_000_000:
+            assert r.key() == oracle.solve_dense(inst).key()
+        n_inf += r.status == wcsp.INFEASIBLE
+    assert n_inf >= 30
+
+
+def test_unit_equals_jump():
+    """Reading R4: advancing by 1 or by the min residual
+     gives identical outputs."""
+    rng = np.random.default_rng(303)
+    for i in range(60):
+        inst = I.random_small(rng, shapes=[(10, 10), (5, 5, 5)], M_range=(5, 80))
+        rj = wcsp.solve(inst, time_mode="jump")
+        ru = wcsp.solve(inst, time_mode="unit")
+        assert rj.key() == ru.key()
+        if rj.status == wcsp.REACHED:
+            assert ru.cycles == rj.F1   # unit mode visits every t = 1..F1
+
+
+def test_removed_vertices_and_multi_sets():
+    rng = np.random.default_rng(404)
+    for i in range(60):
+        inst = I.random_small(rng, shapes=[(12, 12), (6, 6, 6)], M_range=(10, 90), max_sources=6, max_targets=6)
+        pres = (rng.random(inst.N) > 0.15).astype(np.uint8)
+        inst = inst.with_sets(present=pres)
+        if not (inst.maskA & pres).any() or not (inst.maskB & pres).any():
+            continue
+        check(inst)
+
+
+@pytest.mark.parametrize("seed", range(0, 40))
+def test_C1_infeasible_and_C1b(seed):
+    c = I.config_C1(seed)
+    r = wcsp.solve(c)
+    assert r.status == wcsp.INFEASIBLE
+    check(c)
+    check(I.config_C1(seed, 65))
+
+
+def test_determinism_repeated_runs():
+    inst = I.config_face((96, 96), 5, 300)
+    rs = [wcsp.solve(inst, engine=e) for e in ENGINES for _ in range(3)]
+    for r in rs[1:]:
+        assert (r.key(), r.cycles, r.edge_updates, r.phantoms_created, r.relabels, r.triggered, r.arrivals) == \
+               (rs[0].key(), rs[0].cycles, rs[0].edge_updates, rs[0].phantoms_created, rs[0].relabels,
+                rs[0].triggered, rs[0].arrivals)
+
+
+def test_reconstruction_valid_and_optimal():
+    """Reading R12 (PAPER.md:25 corrected): the recovered path is an A->B path
+    with exactly (F1, F2), checked by the oracle's independent path check."""
+    rng = np.random.default_rng(505)
+    done = 0
+    for i in range(80):
+        inst = I.random_small(rng, shapes=[(8, 8), (10, 6), (4, 4, 4)], M_range=(10, 70), max_sources=3,
+                              max_targets=3)
+        if i % 7 == 6:
+            inst = inst.with_M(I.M_INF)
+        o = oracle.solve_pruned(inst)
+        if o.status != oracle.REACHED:
+            continue
+        with wcsp.Solver(inst) as s:
+            path, r = s.reconstruct()
+        assert r.key() == o.key()
+        st, F1, F2 = oracle.validate_path(inst, path)
+        assert st == 0 and F1 == o.F1
+        if inst.M != I.M_INF:
+            assert F2 == o.F2
+        assert path[-1] == o.X and path[-2] == o.Y
+        done += 1
+    assert done >= 40
+
+
+def test_M_infinity_first_passage_and_speedway():
+    for n in (8, 20, 33):
+        for B in ([(0, n)], [(3, n // 2)], [(-n, n), (n, n)]):
+            s = I.speedway_instance(n, B=B)
+            r = wcsp.solve(s)
+            assert r.key() == oracle.solve_lex(s, 2).key()
+            x, y = B[0]
+            if len(B) == 1:
+                assert r.F1 == y + min(y, 2 * abs(x))
+            assert r.phantoms_created == 0                  # M = inf never needs phantoms
+
+
+# --- full BASELINE sizes (configs[1], configs[2]) -------------------------------------------
+
+@pytest.mark.slow
+def test_C2_full_size_binding_M():
+    """configs[1]: 1024^2, U{1..10}, face -> face, M_bind; oracle tier 2 in full."""
+    inst = I.config_face((1024, 1024), 0, I.M_INF)
+    inst = inst.with_M(oracle.m_bind(inst))
+    r = wcsp.solve(inst)
+    o = oracle.solve_pruned(inst)
+    assert r.key() == o.key()
+    assert (r.cycles, r.edge_updates) == (o.cycles, o.work)
+
+
+@pytest.mark.slow
+def test_C3_full_size_M_endpoints_and_properties():
+    """configs[2]: 256^3, face -> face.  Exact at the two M endpoints and M = inf
+    (P3, P4: lexicographic Dijkstra), and at M_bind the sandwich/monotone
+    properties (P5) plus one-step reconstruction consistency (P10)."""
+    inst = I.config_face((256, 256, 256), 0, I.M_INF)
+    lo = oracle.solve_lex(inst, 1)
+    hi = oracle.solve_lex(inst, 0)
+    with wcsp.Solver(inst.with_M(hi.F2 + 1)) as s:
+        assert s.solve().key() == hi.key()
+        s.set_targets(M=lo.F2 + 1)
+        assert s.solve().key() == lo.key()
+        s.set_targets(M=lo.F2)
+        assert s.solve().status == wcsp.INFEASIBLE
+        s.set_targets(M=I.M_INF)
+        assert s.solve().key() == oracle.solve_lex(inst, 2).key()
+        Mb = (lo.F2 + hi.F2) // 2 + 1
+        s.set_targets(M=Mb)
+        rb = s.solve()
+        assert rb.status == wcsp.REACHED and rb.F2 < Mb and hi.F1 <= rb.F1 <= lo.F1
+        s.set_targets(M=Mb + 25)
+        assert s.solve().F1 <= rb.F1

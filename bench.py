@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one step = one complete solve (§4 cycle
+from the initial state to termination) of the bench workload, inputs resident
+in HBM.  Prints ONE JSON line (rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3|C2|C3s]
+    python bench.py --impl reference ...     # the CPU oracle on a bounded sample
+
+Metric (BASELINE.json): active edge-updates/s = sum over cycles of (live active
+edges + live phantom edges) / solve time; also reported: solve
+time, and achieved HBM GB/s of the cycle kernel against MEASURED_PEAKS.json.
+Multi-GPU (N > 1, torchrun): every rank solves its own seed of the workload
+(independent instances, no data-path collective; weak scaling); the time is
+the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "active edge-updates/s and solve time on Z^d cubes; achieved HBM GB/s"
+UNIT = "edge-updates/s"
+WORKLOADS = {
+    "C3": {"shape": (256, 256, 256), "desc": "configs[2]: 3D 256^3 cube, f1,f2 ~ U{1..10}, A = face x=0, "
+                                             "B = face x=255, M = M_bind, 1 GPU"},
+    "C2": {"shape": (1024, 1024), "desc": "configs[1]: 2D 1024^2, f1,f2 ~ U{1..10}, A = left face, B = right face, "
+                                          "M = M_bind"},
+    "C3s": {"shape": (128, 128, 128), "desc": "128^3 cube (reduced C3 for quick runs), M = M_bind"},
+}
+MBIND = os.path.join(ROOT, "paper_1511_06441_b200", "data", "mbind.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def workload_instance(name: str, seed: int):
+    from paper_1511_06441_b200 import instances as I
+    table = json.load(open(MBIND))
+    key = f"{name}/{seed}"
+    if key not in table:
+        key = f"{name}/0"
+    M = table[key]["M_bind"]
+    seed = table[key]["seed"]
+    return I.config_face(WORKLOADS[name]["shape"], seed, M, name=name), table[key]
+
+
+def alg_bytes(r, d: int) -> int:
+    """Algorithmic bytes the method must move (SURVEY §8(d) 'alg', DESIGN.md
+    "Roofline"): 2 B per live lane/phantom per cycle (u8 residual read+write),
+    13 B per arrival, (2d*8 + 22) B per triggered vertex, 8 B per phantom
+    created, 2 B per relabel."""
+    return (2 * r.edge_updates + 13 * r.arrivals + (2 * d * 8 + 22) * r.triggered + 8 * r.phantoms_created
+            + 2 * r.relabels)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_sample(inst, target_s: float = 15.0):
+    """The oracle (tier 2, as it stands) on a bounded sample of the same workload:
+    the first t_limit time units of the same instance, t_limit grown until the
+    run takes about target_s seconds on one host core.  Value = the oracle's own
+    count of flows in flight summed over event times (the same quantity as the
+    metric's numerator, on the oracle's pruned flow set) / CPU seconds."""
+    import oracle
+    t_limit, r, dt = 4, None, 0.0
+    while True:
+        t0 = time.perf_counter()
+        r = oracle.solve_pruned(inst, t_limit=t_limit)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 3 or r.status != oracle.ELIMIT:
+            break
+        t_limit = int(t_limit * max(1.5, min(8.0, target_s / max(dt, 1e-3))))
+    return r, dt, t_limit
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on the host cores, bounded samples."""
+    if rank != 0:
+        return
+    inst, meta = workload_instance(args.workload, 0)
+    import oracle
+    oracle.build()
+    r, dt, t_limit = cpu_sample(inst, target_s=args.ref_seconds)
+    times, work = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        rr = oracle.solve_pruned(inst, t_limit=t_limit)
+        d = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(d)
+            work.append(rr.work)
+    value = sum(work) / sum(times)
+    sample = f"first {t_limit} time units of {args.workload} seed {meta['seed']} (t_final of the full solve ~{meta['F1_lex']}+)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic", "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
+                                            "seed": meta["seed"], "M": inst.M, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--engine", default="persistent", choices=["persistent", "stepped"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1511_06441_b200 import wcsp
+
+    inst, meta = workload_instance(args.workload, rank)
+    d = len(inst.shape)
+    stream = torch.cuda.current_stream()
+    solver = wcsp.Solver(inst, engine=args.engine, stream=stream)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > L2 (126 MB)
+
+    for _ in range(args.warmup):
+        solver.solve()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # timed region: K solves, L2 flushed between steps (outside the events)
+    results, step_ms = [], []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            results.append(solver.solve())
+            ev[i][1].record(stream)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    updates = sum(r.edge_updates for r in results)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        u = torch.tensor([updates], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(u, op=torch.distributed.ReduceOp.SUM)
+        total_ms, updates_all = float(t.item()), float(u.item())
+    else:
+        updates_all = updates
+    value = updates_all / (total_ms / 1000.0)
+
+    # roofline of the dominant kernel (the cycle kernel; one launch per solve)
+    r0 = results[0]
+    cyc_ms = statistics.mean(r.cycle_ms for r in results)
+    ab = alg_bytes(r0, d)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = ab / (cyc_ms / 1000.0) / 1e9
+    traffic = None
+    if os.path.exists(PROFILE_SUMMARY):
+        try:
+            ps = json.load(open(PROFILE_SUMMARY)).get(f"{args.workload}/{args.engine}")
+            traffic = ps["dram_bytes_per_launch"] if ps else None
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": f"k_{args.engine} (cycle kernel, {'1 launch' if args.engine == 'persistent' else '3 launches/cycle'} per solve)",
+                "alg_bytes_per_launch": ab,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback B200_PROFILING.md 6.65 TB/s"}
+
+    # e2e through the C-ABI with host buffers (pinned): H2D of the step's inputs + solve + result read
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(inst, k))).pin_memory()
+               for k in ("f1", "f2", "maskA", "maskB")}
+        host = {k: v.numpy() for k, v in pin.items()}
+        h2d = sum(v.numel() for v in pin.values())
+        e_ms, e_upd = [], 0
+        barrier()
+        for i in range(args.e2e_steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            solver.load(f1=host["f1"], f2=host["f2"], maskA=host["maskA"], maskB=host["maskB"], M=inst.M)
+            rr = solver.solve()
+            b.record(stream)
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+            e_upd += rr.edge_updates
+        et = sum(e_ms)
+        if world > 1:
+            t = torch.tensor([et], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            et = float(t.item())
+            u = torch.tensor([e_upd], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(u, op=torch.distributed.ReduceOp.SUM)
+            e_upd = float(u.item())
+        e2e = {"value": e_upd / (et / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 312, "ms_per_step": et / args.e2e_steps,
+               "path": "wcsp_load (pinned host f1,f2,A,B -> HBM, validate, weight build) + wcsp_solve + result D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r, dt, t_limit = cpu_sample(inst)
+        cpu = {"value": r.work / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle tier 2 (oracle/wcsp_oracle.c orc_pruned) on the first {t_limit} time units of the "
+                         f"same instance ({dt:.1f} s, {r.work} flow-updates, {r.cycles} event times)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
+                       "shape": list(inst.shape), "seed": meta["seed"], "M": inst.M,
+                       "M_bind_from": "paper_1511_06441_b200/data/mbind.json (oracle, scripts/make_mbind.py)",
+                       "engine": args.engine, "l2": "flushed between steps (256 MiB write outside the events)",
+                       "parallelism": f"{world} independent instances (one seed per rank)" if world > 1 else "1 GPU"},
+            "solve_ms": total_ms / args.steps,
+            "solve": {"F1": r0.F1, "F2": r0.F2, "X": r0.X, "Y": r0.Y, "cycles": r0.cycles,
+                      "edge_updates": r0.edge_updates, "arrivals": r0.arrivals, "triggered": r0.triggered,
+                      "phantoms_created": r0.phantoms_created, "relabels": r0.relabels,
+                      "peak_active": r0.peak_active, "peak_phantoms": r0.peak_phantoms,
+                      "cycle_ms": r0.cycle_ms, "device_ms": r0.device_ms},
+            "hbm_gbs_alg": round(achieved, 2),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(sum(r.kernel_launches for r in results)),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -113,6 +113,7 @@ typedef struct {
   int64_t phantom_capacity; /* pool capacity used by the successful run */
   int64_t kernel_launches;  /* CUDA kernels this solve launched */
   double device_ms;         /* device time of the solve (init + cycles), CUDA events */
+  double cycle_ms;          /* device time of the cycle kernels alone (excludes the init kernel) */
 } wcsp_result;
 
 /* One record per cycle when options.trace_cap > 0 (after the cycle ran). */

@@ -65,7 +65,7 @@ struct wcsp_handle {
   unsigned long long* d_cnt = nullptr;               // validation counters
   long long M = 0, M_saved = 0;
   int nsm = 0, coop_blocks = 0, step_blocks = 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
   long long last_cycles = 0;
   long long launches = 0;
 };
@@ -200,6 +200,7 @@ void release(wcsp_handle* h) {
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
   if (h->e0) cudaEventDestroy(h->e0);
   if (h->e1) cudaEventDestroy(h->e1);
+  if (h->em) cudaEventDestroy(h->em);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
 }
 
@@ -296,6 +297,7 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   CK(cudaEventRecord(h->e0, h->stream));
   if ((st = reset_ctl(h)) != WCSP_REACHED) return st;
   if ((st = launch_init(h)) != WCSP_REACHED) return st;
+  CK(cudaEventRecord(h->em, h->stream));
   if (h->opt.engine == WCSP_ENGINE_STEPPED)
     st = run_stepped(h);
   else
@@ -304,9 +306,11 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   CK(cudaEventRecord(h->e1, h->stream));
   CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
-  float ms = 0;
+  float ms = 0, cms = 0;
   CK(cudaEventElapsedTime(&ms, h->e0, h->e1));
+  CK(cudaEventElapsedTime(&cms, h->em, h->e1));
   const Ctl& c = *h->h_ctl;
+  if (c.abort) return fail(WCSP_ECUDA, "persistent kernel: grid barrier watchdog fired (blocks not co-resident?)");
   *status = c.view.status;
   memset(r, 0, sizeof(*r));
   r->F1 = c.F1;
@@ -327,6 +331,7 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   r->phantom_capacity = (long long)h->pool_cap;
   r->kernel_launches = h->launches;
   r->device_ms = ms;
+  r->cycle_ms = cms;
   h->last_cycles = c.cycles;
   if (*status == WCSP_EOVERFLOW) r->phantom_capacity = c.need_pool;
   return WCSP_REACHED;
@@ -426,6 +431,7 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
   CKC(cudaMalloc(&h->trace, std::max<long long>(1, opt.trace_cap) * sizeof(TraceRec)));
   CKC(cudaEventCreate(&h->e0));
   CKC(cudaEventCreate(&h->e1));
+  CKC(cudaEventCreate(&h->em));
   const unsigned long long cap = opt.phantom_capacity > 0 ? (unsigned long long)opt.phantom_capacity
                                                           : std::max<unsigned long long>(4 * N, 1ull << 20);
   CKH(alloc_pool(h, cap));

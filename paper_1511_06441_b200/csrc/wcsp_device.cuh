@@ -61,6 +61,7 @@ struct Ctl {
   View view;
   Acc acc[3];
   unsigned long long bar;          // grid barrier arrivals (persistent engine)
+  unsigned abort, pad_;            // barrier watchdog fired
   long long F1, F2, X, Y;
   long long via;
   long long cycles, edge_updates, arrivals, triggered, created, relabels;
@@ -462,15 +463,35 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   return v;
 }
 
-__device__ __forceinline__ void grid_sync(unsigned long long* bar, unsigned long long target) {
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Returns false if the barrier was abandoned (watchdog: a block missing for
+// BARRIER_TIMEOUT_NS sets ctl->abort; every waiting block then gives up).
+constexpr unsigned long long BARRIER_TIMEOUT_NS = 20ull * 1000000000ull;
+
+__device__ __forceinline__ bool grid_sync(Ctl* ctl, unsigned long long target, Smem& sm) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    atomicAdd(bar, 1ull);
-    while (ld_acquire(bar) < target) __nanosleep(40);
+    atomicAdd(&ctl->bar, 1ull);
+    const unsigned long long t0 = globaltimer_ns();
+    unsigned ok = 1;
+    while (ld_acquire(&ctl->bar) < target) {
+      __nanosleep(40);
+      if (*(volatile unsigned*)&ctl->abort) { ok = 0; break; }
+      if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&ctl->abort, 1u); ok = 0; break; }
+    }
     __threadfence();
+    sm.base = ok;
   }
   __syncthreads();
+  const bool ok = sm.base != 0;
+  __syncthreads();
+  return ok;
 }
 
 __device__ __forceinline__ void load_view(const Dev& s, Smem& sm, View& v) {
@@ -506,7 +527,7 @@ __global__ void __launch_bounds__(THREADS) k_persistent(Dev s) {
       if (blockIdx.x == 0 && threadIdx.x == 0) reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
       phase_sweep<D>(s, v, sm);
       target += G;
-      grid_sync(&s.ctl->bar, target);
+      if (!grid_sync(s.ctl, target, sm)) return;
     }
     if (threadIdx.x == 0) {
       sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
@@ -519,7 +540,7 @@ __global__ void __launch_bounds__(THREADS) k_persistent(Dev s) {
     if (!bhit) {                                   // S5 precedes S6: the final cycle skips the treat
       phase_treat<D>(s, v, sm, n_trig);
       target += G;
-      grid_sync(&s.ctl->bar, target);
+      if (!grid_sync(s.ctl, target, sm)) return;
     }
     if (threadIdx.x == 0) {
       View nv = v;
@@ -534,7 +555,7 @@ __global__ void __launch_bounds__(THREADS) k_persistent(Dev s) {
            i += (unsigned long long)gridDim.x * THREADS)
         s.temp[i] = 0ull;
       target += G;
-      grid_sync(&s.ctl->bar, target);
+      if (!grid_sync(s.ctl, target, sm)) return;
     }
   }
 }

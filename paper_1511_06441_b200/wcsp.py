@@ -56,7 +56,8 @@ class _Result(ctypes.Structure):
                 ("triggered", ctypes.c_int64), ("phantoms_created", ctypes.c_int64),
                 ("relabels", ctypes.c_int64), ("peak_active", ctypes.c_int64),
                 ("peak_phantoms", ctypes.c_int64), ("phantom_capacity", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64), ("device_ms", ctypes.c_double)]
+                ("kernel_launches", ctypes.c_int64), ("device_ms", ctypes.c_double),
+                ("cycle_ms", ctypes.c_double)]
 
 
 TRACE_FIELDS = ["t", "delta", "active_vertices", "live_lanes", "phantoms", "triggered", "arrivals",
@@ -129,6 +130,7 @@ class Result:
     phantom_capacity: int = 0
     kernel_launches: int = 0
     device_ms: float = 0.0
+    cycle_ms: float = 0.0
 
     def key(self):
         """Outputs compared bit-exactly with the oracle: (status, F1, F2, X, Y)."""

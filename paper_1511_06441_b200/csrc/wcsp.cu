@@ -53,8 +53,9 @@ struct wcsp_handle {
   bool present_all = true, present_all_saved = true;
   void* wt = nullptr;
   void* res = nullptr;
-  unsigned short* label = nullptr;
-  unsigned long long* temp = nullptr;
+  unsigned long long* sw = nullptr;                 // vertex state words (label | temp)
+  BArr* barr = nullptr;                              // arrivals at targets (terminating cycle)
+  unsigned barr_cap = 0;
   unsigned* act[2] = {nullptr, nullptr};
   unsigned* trig = nullptr;
   unsigned long long* pool[2] = {nullptr, nullptr};
@@ -93,8 +94,9 @@ Dev make_dev(const wcsp_handle* h) {
   }
   s.wt = h->wt;
   s.res = h->res;
-  s.label = h->label;
-  s.temp = h->temp;
+  s.sw = h->sw;
+  s.barr = h->barr;
+  s.barr_cap = h->barr_cap;
   s.act[0] = h->act[0]; s.act[1] = h->act[1];
   s.trig = h->trig;
   s.pool[0] = h->pool[0]; s.pool[1] = h->pool[1];
@@ -145,6 +147,15 @@ wcsp_status validate_device(wcsp_handle* h, const uint8_t* f1, const uint8_t* f2
   if (c[1] == 0) return fail(WCSP_EINVAL, "B is empty (among present vertices)");
   if (c[2] != 0) return fail(WCSP_EINVAL, "A and B intersect in %llu vertices", c[2]);
   if (c[3] != 0) return fail(WCSP_EINVAL, "%llu present edges have f1 > 0 and f2 = 0", c[3]);
+  // per cycle a target receives at most one lane and one phantom per half-edge: 2 * 2d arrivals
+  const unsigned long long need = std::max<unsigned long long>(64, 4ull * h->d * c[1]);
+  if (need > h->barr_cap) {
+    if (h->barr) cudaFree(h->barr);
+    h->barr = nullptr;
+    h->barr_cap = 0;
+    CK(cudaMalloc(&h->barr, need * sizeof(BArr)));
+    h->barr_cap = (unsigned)need;
+  }
   return WCSP_REACHED;
 }
 
@@ -193,7 +204,7 @@ wcsp_status load_problem(wcsp_handle* h, const wcsp_problem* p) {
 
 void release(wcsp_handle* h) {
   void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->d_maskB_saved, h->d_present_saved,
-                  h->wt, h->res, h->label, h->temp, h->act[0], h->act[1], h->trig, h->pool[0], h->pool[1],
+                  h->wt, h->res, h->sw, h->barr, h->act[0], h->act[1], h->trig, h->pool[0], h->pool[1],
                   h->ctl, h->trace, h->d_cnt};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -269,7 +280,9 @@ wcsp_status run_stepped(wcsp_handle* h) {
     CK(cudaStreamSynchronize(h->stream));
     const int st = h->h_ctl->view.status;
     if (st == ST_WRAP) {
-      CK(cudaMemsetAsync(h->temp, 0, h->N * sizeof(unsigned long long), h->stream));
+      k_clear_temps<<<h->step_blocks, THREADS, 0, h->stream>>>(s);
+      h->launches += 1;
+      CK(cudaGetLastError());
       const int run = ST_RUNNING;
       CK(cudaMemcpyAsync(&h->ctl->view.status, &run, sizeof(int), cudaMemcpyHostToDevice, h->stream));
       CK(cudaStreamSynchronize(h->stream));
@@ -411,7 +424,11 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
   CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, 0));
   if (per_sm < 1) CKH(fail(WCSP_ECUDA, "persistent kernel cannot be resident"));
   h->coop_blocks = per_sm * h->nsm;
-  h->step_blocks = per_sm * h->nsm;
+  int per_sm_step = 0;
+  void* sfn = p->d == 1 ? reinterpret_cast<void*>(&k_sweep<1>) : p->d == 2 ? reinterpret_cast<void*>(&k_sweep<2>)
+            : p->d == 3 ? reinterpret_cast<void*>(&k_sweep<3>) : reinterpret_cast<void*>(&k_sweep<4>);
+  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_step, sfn, THREADS, 0));
+  h->step_blocks = std::max(1, per_sm_step) * h->nsm;
   const size_t fb = (size_t)h->d * N;
   CKC(cudaMalloc(&h->d_f1, fb));
   CKC(cudaMalloc(&h->d_f2, fb));
@@ -420,8 +437,7 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
   CKC(cudaMalloc(&h->d_present, N));
   CKC(cudaMalloc(&h->wt, N * 2 * lane_bytes(h->d)));
   CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
-  CKC(cudaMalloc(&h->label, N * sizeof(unsigned short)));
-  CKC(cudaMalloc(&h->temp, N * sizeof(unsigned long long)));
+  CKC(cudaMalloc(&h->sw, N * sizeof(unsigned long long)));
   CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));
   CKC(cudaMalloc(&h->act[1], N * sizeof(unsigned)));
   CKC(cudaMalloc(&h->trig, N * sizeof(unsigned)));

@@ -167,7 +167,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
-    ap.add_argument("--engine", default="persistent", choices=["persistent", "stepped"])
+    ap.add_argument("--engine", default="persistent", choices=["persistent", "stepped", "wheel", "wheel_stepped"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -238,7 +238,7 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": f"k_{args.engine} (cycle kernel, {'1 launch' if args.engine == 'persistent' else '3 launches/cycle'} per solve)",
+                "kernel": {"persistent": "k_persistent<D>", "wheel": "k_wheel_persistent<D>"}.get(args.engine, "k_*<D> (stepped: 3 launches per cycle)") + " (cycle kernel)",
                 "alg_bytes_per_launch": ab,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback B200_PROFILING.md 6.65 TB/s"}
 

@@ -62,8 +62,12 @@ typedef enum {
 enum { WCSP_MEM_HOST = 0, WCSP_MEM_DEVICE = 1 };
 enum { WCSP_JUMP = 0,             /* advance t by the min live residual */
        WCSP_UNIT = 1 };           /* advance t by 1 — identical outputs */
-enum { WCSP_ENGINE_PERSISTENT = 0,/* one cooperative kernel runs every cycle (device-side termination) */
-       WCSP_ENGINE_STEPPED = 1 }; /* one kernel per phase, host polls termination every few cycles */
+enum { WCSP_ENGINE_PERSISTENT = 0,   /* sweep engine: residual countdown on the active list + phantom pool
+                                        (PAPER.md:157, :173), one cooperative kernel runs every cycle */
+       WCSP_ENGINE_STEPPED = 1,      /* sweep engine, one kernel per phase, host polls termination */
+       WCSP_ENGINE_WHEEL = 2,        /* timing-wheel engine: live edges stored by arrival time, written
+                                        once and read once (same outputs and counters), persistent */
+       WCSP_ENGINE_WHEEL_STEPPED = 3 };
 
 /* Problem statement.  Validation (wcsp_create / wcsp_load):
  *  d in 1..4, every shape[k] >= 1, N <= 2^30;  A and B non-empty among the
@@ -85,11 +89,12 @@ typedef struct {
 
 typedef struct {
   int32_t time_mode;        /* WCSP_JUMP (default) | WCSP_UNIT */
-  int32_t engine;           /* WCSP_ENGINE_PERSISTENT (default) | WCSP_ENGINE_STEPPED */
+  int32_t engine;           /* WCSP_ENGINE_* (default 0 = sweep, persistent) */
   int32_t demote_twin;      /* reserved (twin re-sourcing): must be 0 in this version */
   int32_t device;           /* CUDA device ordinal */
   int64_t cycle_budget;     /* 0 = unlimited; else WCSP_EBUDGET after that many cycles */
-  int64_t phantom_capacity; /* records per pool buffer; 0 = auto (4N, min 2^20); grown on overflow */
+  int64_t phantom_capacity; /* sweep: phantom records per pool buffer; wheel: event-ring slots;
+                               0 = auto (4N, min 2^20); grown automatically on overflow */
   int64_t trace_cap;        /* per-cycle trace records kept (0 = off) */
   void* stream;             /* cudaStream_t or NULL (the library creates one) */
 } wcsp_options;

@@ -1,7 +1,8 @@
 // wcsp.cu — host side of the C-ABI (include/wcsp.h): handle, validation,
-// engines (persistent cooperative kernel / stepped kernels), reconstruction.
+// engines (sweep / timing wheel, each persistent or stepped), reconstruction.
 #include "wcsp.h"
 #include "wcsp_device.cuh"
+#include "wcsp_wheel.cuh"
 
 #include <cuda_runtime.h>
 
@@ -28,13 +29,16 @@ wcsp_status fail(wcsp_status st, const char* fmt, ...) {
   return st;
 }
 
-#define CK(call)                                                                             \
-  do {                                                                                       \
-    cudaError_t e_ = (call);                                                                 \
-    if (e_ != cudaSuccess)                                                                   \
+#define CK(call)                                                                                \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
       return fail(e_ == cudaErrorMemoryAllocation ? WCSP_ENOMEM : WCSP_ECUDA, "%s: %s (%s:%d)", \
-                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                           \
   } while (0)
+
+bool is_wheel(int engine) { return engine == WCSP_ENGINE_WHEEL || engine == WCSP_ENGINE_WHEEL_STEPPED; }
+bool is_stepped(int engine) { return engine == WCSP_ENGINE_STEPPED || engine == WCSP_ENGINE_WHEEL_STEPPED; }
 
 }  // namespace
 
@@ -49,23 +53,29 @@ struct wcsp_handle {
   // device buffers
   uint8_t *d_f1 = nullptr, *d_f2 = nullptr;          // staging of host inputs [d][N]
   uint8_t *d_maskA = nullptr, *d_maskB = nullptr, *d_present = nullptr;
-  uint8_t *d_maskB_saved = nullptr, *d_present_saved = nullptr;  // reconstruction
-  bool present_all = true, present_all_saved = true;
+  bool present_all = true;
   void* wt = nullptr;
-  void* res = nullptr;
-  unsigned long long* sw = nullptr;                 // vertex state words (label | temp)
+  void* res = nullptr;                               // sweep engines only
+  unsigned long long* sw = nullptr;                  // vertex state words (label | temp)
+  unsigned* tbits = nullptr;                         // triggered bitmap
+  unsigned nwords = 0;
   BArr* barr = nullptr;                              // arrivals at targets (terminating cycle)
   unsigned barr_cap = 0;
-  unsigned* act[2] = {nullptr, nullptr};
-  unsigned* trig = nullptr;
-  unsigned long long* pool[2] = {nullptr, nullptr};
+  unsigned* act[2] = {nullptr, nullptr};             // sweep engines only
+  unsigned long long* pool[2] = {nullptr, nullptr};  // sweep engines only
   unsigned long long pool_cap = 0;
+  unsigned long long* ev = nullptr;                  // wheel engines only
+  unsigned long long ev_cap = 0;
+  unsigned long long* bdesc = nullptr;
+  unsigned* bcounts = nullptr;                       // bndesc | bnev | bnlane (3 x 256)
+  unsigned dcap = 0;
+  int f1max = 255;
   Ctl* ctl = nullptr;
   Ctl* h_ctl = nullptr;                              // pinned
   TraceRec* trace = nullptr;
   unsigned long long* d_cnt = nullptr;               // validation counters
-  long long M = 0, M_saved = 0;
-  int nsm = 0, coop_blocks = 0, step_blocks = 0;
+  long long M = 0;
+  int nsm = 0, grid = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
   long long last_cycles = 0;
   long long launches = 0;
@@ -76,7 +86,30 @@ namespace {
 size_t lane_bytes(int d) { return d <= 2 ? 4 : 8; }
 
 template <int D>
-void* persistent_fn() { return reinterpret_cast<void*>(&k_persistent<D>); }
+void* cycle_fn(int engine) {
+  switch (engine) {
+    case WCSP_ENGINE_PERSISTENT: return reinterpret_cast<void*>(&k_persistent<D>);
+    case WCSP_ENGINE_STEPPED: return reinterpret_cast<void*>(&k_sweep<D>);
+    case WCSP_ENGINE_WHEEL: return reinterpret_cast<void*>(&k_wheel_persistent<D>);
+    default: return reinterpret_cast<void*>(&k_wheel_treat<D>);
+  }
+}
+void* cycle_fn_d(int d, int engine) {
+  return d == 1 ? cycle_fn<1>(engine) : d == 2 ? cycle_fn<2>(engine) : d == 3 ? cycle_fn<3>(engine) : cycle_fn<4>(engine);
+}
+
+template <int D>
+cudaError_t set_smem_attrs() {
+  const int bytes = (int)sizeof(Smem);
+  void* fns[] = {reinterpret_cast<void*>(&k_persistent<D>), reinterpret_cast<void*>(&k_sweep<D>),
+                 reinterpret_cast<void*>(&k_treat<D>), reinterpret_cast<void*>(&k_wheel_persistent<D>),
+                 reinterpret_cast<void*>(&k_wheel_fire<D>), reinterpret_cast<void*>(&k_wheel_treat<D>)};
+  for (void* f : fns) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 
 Dev make_dev(const wcsp_handle* h) {
   Dev s{};
@@ -95,12 +128,13 @@ Dev make_dev(const wcsp_handle* h) {
   s.wt = h->wt;
   s.res = h->res;
   s.sw = h->sw;
-  s.barr = h->barr;
-  s.barr_cap = h->barr_cap;
+  s.tbits = h->tbits;
+  s.nwords = h->nwords;
   s.act[0] = h->act[0]; s.act[1] = h->act[1];
-  s.trig = h->trig;
   s.pool[0] = h->pool[0]; s.pool[1] = h->pool[1];
   s.pool_cap = h->pool_cap;
+  s.barr = h->barr;
+  s.barr_cap = h->barr_cap;
   s.ctl = h->ctl;
   s.trace = h->trace;
   s.trace_cap = h->opt.trace_cap;
@@ -108,6 +142,15 @@ Dev make_dev(const wcsp_handle* h) {
   s.unit = h->opt.time_mode == WCSP_UNIT;
   s.minf = h->M == WCSP_M_INF;
   s.M = (int)(h->M == WCSP_M_INF ? 1 : h->M);
+  s.ev = h->ev;
+  s.ev_mask = h->ev_cap ? h->ev_cap - 1 : 0;
+  s.bdesc = h->bdesc;
+  s.bndesc = h->bcounts;
+  s.bnev = h->bcounts ? h->bcounts + WHEEL : nullptr;
+  s.bnlane = h->bcounts ? h->bcounts + 2 * WHEEL : nullptr;
+  s.dcap = h->dcap;
+  s.f1max = h->f1max;
+  s.nblocks = (unsigned)h->grid;
   return s;
 }
 
@@ -119,6 +162,31 @@ wcsp_status alloc_pool(wcsp_handle* h, unsigned long long cap) {
   CK(cudaMalloc(&h->pool[0], cap * sizeof(unsigned long long)));
   CK(cudaMalloc(&h->pool[1], cap * sizeof(unsigned long long)));
   h->pool_cap = cap;
+  return WCSP_REACHED;
+}
+
+unsigned long long pow2_at_least(unsigned long long x) {
+  unsigned long long p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+wcsp_status alloc_ring(wcsp_handle* h, unsigned long long cap) {
+  if (h->ev) cudaFree(h->ev);
+  h->ev = nullptr;
+  h->ev_cap = 0;
+  cap = pow2_at_least(cap);
+  CK(cudaMalloc(&h->ev, cap * sizeof(unsigned long long)));
+  h->ev_cap = cap;
+  return WCSP_REACHED;
+}
+
+wcsp_status alloc_desc(wcsp_handle* h, unsigned dcap) {
+  if (h->bdesc) cudaFree(h->bdesc);
+  h->bdesc = nullptr;
+  h->dcap = 0;
+  CK(cudaMalloc(&h->bdesc, (size_t)WHEEL * dcap * sizeof(unsigned long long)));
+  h->dcap = dcap;
   return WCSP_REACHED;
 }
 
@@ -135,18 +203,19 @@ wcsp_status check_M(long long M) {
 }
 
 wcsp_status validate_device(wcsp_handle* h, const uint8_t* f1, const uint8_t* f2) {
-  CK(cudaMemsetAsync(h->d_cnt, 0, 4 * sizeof(unsigned long long), h->stream));
+  CK(cudaMemsetAsync(h->d_cnt, 0, 5 * sizeof(unsigned long long), h->stream));
   k_validate<<<grid_for(h, h->N), THREADS, 0, h->stream>>>(h->N, h->d, h->shape[0], h->shape[1], h->shape[2],
                                                           h->shape[3], f1, f2, h->d_maskA, h->d_maskB,
                                                           h->present_all ? nullptr : h->d_present, h->d_cnt);
   CK(cudaGetLastError());
-  unsigned long long c[4];
+  unsigned long long c[5];
   CK(cudaMemcpyAsync(c, h->d_cnt, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   if (c[0] == 0) return fail(WCSP_EINVAL, "A is empty (among present vertices)");
   if (c[1] == 0) return fail(WCSP_EINVAL, "B is empty (among present vertices)");
   if (c[2] != 0) return fail(WCSP_EINVAL, "A and B intersect in %llu vertices", c[2]);
   if (c[3] != 0) return fail(WCSP_EINVAL, "%llu present edges have f1 > 0 and f2 = 0", c[3]);
+  h->f1max = std::max<int>(1, (int)c[4]);
   // per cycle a target receives at most one lane and one phantom per half-edge: 2 * 2d arrivals
   const unsigned long long need = std::max<unsigned long long>(64, 4ull * h->d * c[1]);
   if (need > h->barr_cap) {
@@ -203,9 +272,9 @@ wcsp_status load_problem(wcsp_handle* h, const wcsp_problem* p) {
 }
 
 void release(wcsp_handle* h) {
-  void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->d_maskB_saved, h->d_present_saved,
-                  h->wt, h->res, h->sw, h->barr, h->act[0], h->act[1], h->trig, h->pool[0], h->pool[1],
-                  h->ctl, h->trace, h->d_cnt};
+  void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->tbits, h->barr,
+                  h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
+                  h->d_cnt};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -216,17 +285,14 @@ void release(wcsp_handle* h) {
 }
 
 wcsp_status reset_ctl(wcsp_handle* h) {
-  Ctl c;
-  memset(&c, 0, sizeof(c));
-  c.view.t = 0;
-  c.view.c = 0;
+  memset(h->h_ctl, 0, sizeof(Ctl));
+  Ctl& c = *h->h_ctl;
   c.view.stamp = stamp_of(0);
-  c.view.delta = 0;
-  c.view.cur = 0;
   c.view.status = ST_RUNNING;
+  c.view.region = 256;
   for (int i = 0; i < 3; ++i) c.acc[i].dmin = 0xFFFFFFFFu;
-  *h->h_ctl = c;
   CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
+  if (is_wheel(h->opt.engine)) CK(cudaMemsetAsync(h->bcounts, 0, 3 * WHEEL * sizeof(unsigned), h->stream));
   return WCSP_REACHED;
 }
 
@@ -242,24 +308,25 @@ wcsp_status launch_init(wcsp_handle* h) {
 
 wcsp_status run_persistent(wcsp_handle* h) {
   Dev s = make_dev(h);
-  void* fn = nullptr;
-  switch (h->d) {
-    case 1: fn = persistent_fn<1>(); break;
-    case 2: fn = persistent_fn<2>(); break;
-    case 3: fn = persistent_fn<3>(); break;
-    default: fn = persistent_fn<4>(); break;
-  }
   void* args[] = {&s};
-  CK(cudaLaunchCooperativeKernel(fn, dim3(h->coop_blocks), dim3(THREADS), args, 0, h->stream));
+  CK(cudaLaunchCooperativeKernel(cycle_fn_d(h->d, h->opt.engine), dim3(h->grid), dim3(THREADS), args, sizeof(Smem),
+                                 h->stream));
   h->launches += 1;
   return WCSP_REACHED;
 }
 
 template <int D>
 void launch_cycle(wcsp_handle* h, const Dev& s) {
-  k_sweep<D><<<h->step_blocks, THREADS, 0, h->stream>>>(s);
-  k_treat<D><<<h->step_blocks, THREADS, 0, h->stream>>>(s);
-  k_decide<<<1, 32, 0, h->stream>>>(s);
+  const size_t sm = sizeof(Smem);
+  if (is_wheel(h->opt.engine)) {
+    k_wheel_fire<D><<<h->grid, THREADS, sm, h->stream>>>(s);
+    k_wheel_treat<D><<<h->grid, THREADS, sm, h->stream>>>(s);
+    k_wheel_decide<<<1, 32, 0, h->stream>>>(s);
+  } else {
+    k_sweep<D><<<h->grid, THREADS, sm, h->stream>>>(s);
+    k_treat<D><<<h->grid, THREADS, sm, h->stream>>>(s);
+    k_decide<<<1, 32, 0, h->stream>>>(s);
+  }
 }
 
 wcsp_status run_stepped(wcsp_handle* h) {
@@ -279,8 +346,9 @@ wcsp_status run_stepped(wcsp_handle* h) {
     CK(cudaMemcpyAsync(&h->h_ctl->view, &h->ctl->view, sizeof(View), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     const int st = h->h_ctl->view.status;
-    if (st == ST_WRAP) {
-      k_clear_temps<<<h->step_blocks, THREADS, 0, h->stream>>>(s);
+    if (st == ST_WRAP) {               // maintenance pass (stamp wrap / texp refresh), then continue
+      if (is_wheel(h->opt.engine)) k_wheel_maintain<<<h->grid, THREADS, 0, h->stream>>>(s);
+      else k_clear_temps<<<h->grid, THREADS, 0, h->stream>>>(s);
       h->launches += 1;
       CK(cudaGetLastError());
       const int run = ST_RUNNING;
@@ -311,10 +379,7 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   if ((st = reset_ctl(h)) != WCSP_REACHED) return st;
   if ((st = launch_init(h)) != WCSP_REACHED) return st;
   CK(cudaEventRecord(h->em, h->stream));
-  if (h->opt.engine == WCSP_ENGINE_STEPPED)
-    st = run_stepped(h);
-  else
-    st = run_persistent(h);
+  st = is_stepped(h->opt.engine) ? run_stepped(h) : run_persistent(h);
   if (st != WCSP_REACHED) return st;
   CK(cudaEventRecord(h->e1, h->stream));
   CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
@@ -341,7 +406,7 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   r->relabels = c.relabels;
   r->peak_active = c.peak_active;
   r->peak_phantoms = c.peak_phantoms;
-  r->phantom_capacity = (long long)h->pool_cap;
+  r->phantom_capacity = (long long)(is_wheel(h->opt.engine) ? h->ev_cap : h->pool_cap);
   r->kernel_launches = h->launches;
   r->device_ms = ms;
   r->cycle_ms = cms;
@@ -353,16 +418,21 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
 wcsp_status solve_impl(wcsp_handle* h, wcsp_result* out) {
   wcsp_result r;
   int status = ST_RUNNING;
-  for (int attempt = 0; attempt < 4; ++attempt) {
+  for (int attempt = 0; attempt < 6; ++attempt) {
     wcsp_status st = solve_once(h, &r, &status);
     if (st != WCSP_REACHED) return st;
     if (status != WCSP_EOVERFLOW) break;
-    // phantom pool overflow: grow to the observed need and re-run (device flag -> host retry)
-    const unsigned long long need = (unsigned long long)r.phantom_capacity;
-    const unsigned long long cap = std::max(need + need / 2, h->pool_cap * 2);
-    if ((st = alloc_pool(h, cap)) != WCSP_REACHED) return st;
+    // overflow of a device structure: grow it and re-run (device flag -> host retry)
+    const long long need = r.phantom_capacity;
+    if (is_wheel(h->opt.engine)) {
+      if (need == -2) st = alloc_desc(h, h->dcap * 2);
+      else st = alloc_ring(h, std::max<unsigned long long>((unsigned long long)need + need / 2, h->ev_cap * 2));
+    } else {
+      st = alloc_pool(h, std::max<unsigned long long>((unsigned long long)need + need / 2, h->pool_cap * 2));
+    }
+    if (st != WCSP_REACHED) return st;
   }
-  if (status == WCSP_EOVERFLOW) return fail(WCSP_EOVERFLOW, "phantom pool overflow (need %lld)", r.phantom_capacity);
+  if (status == WCSP_EOVERFLOW) return fail(WCSP_EOVERFLOW, "phantom/event storage overflow after retries");
   if (status == WCSP_EBUDGET) { *out = r; return fail(WCSP_EBUDGET, "cycle budget %lld exceeded", h->opt.cycle_budget); }
   if (status != WCSP_REACHED && status != WCSP_INFEASIBLE) return fail(WCSP_ECUDA, "solver ended in state %d", status);
   *out = r;
@@ -375,7 +445,9 @@ extern "C" {
 
 const char* wcsp_last_error(void) { return g_err.c_str(); }
 
-const char* wcsp_version(void) { return "wcsp-b200 0.1 (sm_100a; persistent + stepped engines)"; }
+const char* wcsp_version(void) {
+  return "wcsp-b200 0.2 (sm_100a; engines: sweep/wheel x persistent/stepped)";
+}
 
 wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handle** out) {
   if (!p || !out) return fail(WCSP_EINVAL, "problem and out must be non-NULL");
@@ -392,7 +464,8 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
   if (o) opt = *o;
   if (opt.demote_twin) return fail(WCSP_EINVAL, "demote_twin is reserved in this version (must be 0)");
   if (opt.time_mode != WCSP_JUMP && opt.time_mode != WCSP_UNIT) return fail(WCSP_EINVAL, "bad time_mode");
-  if (opt.engine != WCSP_ENGINE_PERSISTENT && opt.engine != WCSP_ENGINE_STEPPED) return fail(WCSP_EINVAL, "bad engine");
+  if (opt.engine < WCSP_ENGINE_PERSISTENT || opt.engine > WCSP_ENGINE_WHEEL_STEPPED)
+    return fail(WCSP_EINVAL, "bad engine %d", opt.engine);
   if (opt.trace_cap < 0 || opt.cycle_budget < 0 || opt.phantom_capacity < 0) return fail(WCSP_EINVAL, "negative option");
 
   wcsp_handle* h = new wcsp_handle();
@@ -400,6 +473,7 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
   h->d = p->d;
   for (int k = 0; k < 4; ++k) h->shape[k] = k < p->d ? p->shape[k] : 1;
   h->N = N;
+  h->nwords = (unsigned)((N + 31) / 32);
   h->dev = opt.device;
 #define CKH(call)                       \
   do {                                  \
@@ -419,16 +493,16 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
     h->own_stream = true;
   }
   CKC(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  switch (p->d) {
+    case 1: CKC(set_smem_attrs<1>()); break;
+    case 2: CKC(set_smem_attrs<2>()); break;
+    case 3: CKC(set_smem_attrs<3>()); break;
+    default: CKC(set_smem_attrs<4>()); break;
+  }
   int per_sm = 0;
-  void* fn = p->d == 1 ? persistent_fn<1>() : p->d == 2 ? persistent_fn<2>() : p->d == 3 ? persistent_fn<3>() : persistent_fn<4>();
-  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, 0));
-  if (per_sm < 1) CKH(fail(WCSP_ECUDA, "persistent kernel cannot be resident"));
-  h->coop_blocks = per_sm * h->nsm;
-  int per_sm_step = 0;
-  void* sfn = p->d == 1 ? reinterpret_cast<void*>(&k_sweep<1>) : p->d == 2 ? reinterpret_cast<void*>(&k_sweep<2>)
-            : p->d == 3 ? reinterpret_cast<void*>(&k_sweep<3>) : reinterpret_cast<void*>(&k_sweep<4>);
-  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_step, sfn, THREADS, 0));
-  h->step_blocks = std::max(1, per_sm_step) * h->nsm;
+  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_fn_d(p->d, opt.engine), THREADS, sizeof(Smem)));
+  if (per_sm < 1) CKH(fail(WCSP_ECUDA, "cycle kernel cannot be resident"));
+  h->grid = per_sm * h->nsm;
   const size_t fb = (size_t)h->d * N;
   CKC(cudaMalloc(&h->d_f1, fb));
   CKC(cudaMalloc(&h->d_f2, fb));
@@ -436,21 +510,27 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
   CKC(cudaMalloc(&h->d_maskB, N));
   CKC(cudaMalloc(&h->d_present, N));
   CKC(cudaMalloc(&h->wt, N * 2 * lane_bytes(h->d)));
-  CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
   CKC(cudaMalloc(&h->sw, N * sizeof(unsigned long long)));
-  CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));
-  CKC(cudaMalloc(&h->act[1], N * sizeof(unsigned)));
-  CKC(cudaMalloc(&h->trig, N * sizeof(unsigned)));
+  CKC(cudaMalloc(&h->tbits, (size_t)h->nwords * sizeof(unsigned)));
   CKC(cudaMalloc(&h->ctl, sizeof(Ctl)));
   CKC(cudaMallocHost(&h->h_ctl, sizeof(Ctl)));
-  CKC(cudaMalloc(&h->d_cnt, 4 * sizeof(unsigned long long)));
+  CKC(cudaMalloc(&h->d_cnt, 5 * sizeof(unsigned long long)));
   CKC(cudaMalloc(&h->trace, std::max<long long>(1, opt.trace_cap) * sizeof(TraceRec)));
   CKC(cudaEventCreate(&h->e0));
   CKC(cudaEventCreate(&h->e1));
   CKC(cudaEventCreate(&h->em));
   const unsigned long long cap = opt.phantom_capacity > 0 ? (unsigned long long)opt.phantom_capacity
                                                           : std::max<unsigned long long>(4 * N, 1ull << 20);
-  CKH(alloc_pool(h, cap));
+  if (is_wheel(opt.engine)) {
+    CKH(alloc_ring(h, std::max<unsigned long long>(cap, (unsigned long long)h->grid * 2 * 4096)));
+    CKH(alloc_desc(h, (unsigned)std::max<unsigned long long>(8192, 16ull * h->grid)));
+    CKC(cudaMalloc(&h->bcounts, 3 * WHEEL * sizeof(unsigned)));
+  } else {
+    CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
+    CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));
+    CKC(cudaMalloc(&h->act[1], N * sizeof(unsigned)));
+    CKH(alloc_pool(h, cap));
+  }
   CKH(load_problem(h, p));
 #undef CKC
 #undef CKH
@@ -529,8 +609,7 @@ wcsp_status wcsp_reconstruct(wcsp_handle* h, int64_t* path, int64_t cap, int64_t
     if (B[v]) work[v] = 0;
   std::vector<uint8_t> onlyY(N, 0);
   auto edge_f = [&](long long u, long long v, int* f1, int* f2) -> wcsp_status {
-    // weight record of u, lane toward v
-    const int lane = x_lane_of(h, u, v);
+    const int lane = x_lane_of(h, u, v);   // weight record of u, lane toward v
     if (lane < 0) return fail(WCSP_EMISMATCH, "reconstruction: %lld and %lld are not lattice neighbours", u, v);
     const size_t lb = lane_bytes(h->d);
     unsigned char rec[16];
@@ -547,7 +626,7 @@ wcsp_status wcsp_reconstruct(wcsp_handle* h, int64_t* path, int64_t cap, int64_t
     // B' = {Y}, M' = F2 - f2(x) + 1 (reading R12), V' = V \ (B u earlier targets)
     std::fill(onlyY.begin(), onlyY.end(), 0);
     onlyY[(size_t)Y] = 1;
-    const long long Mp = h->M == WCSP_M_INF ? WCSP_M_INF : F2 - f2x + 1;
+    const long long Mp = saved_M == WCSP_M_INF ? WCSP_M_INF : F2 - f2x + 1;
     CK(cudaMemcpyAsync(h->d_maskB, onlyY.data(), N, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_present, work.data(), N, cudaMemcpyHostToDevice, h->stream));
     h->present_all = false;
@@ -565,7 +644,6 @@ wcsp_status wcsp_reconstruct(wcsp_handle* h, int64_t* path, int64_t cap, int64_t
     rev.push_back(Y);
     work[(size_t)Y] = 0;
     X = Y; Y = r.Y; F1 = r.F1; F2 = r.F2;
-    if (saved_M == WCSP_M_INF) F2 = -1;
   }
   if (out == WCSP_REACHED) rev.push_back(Y);
   // restore the loaded problem

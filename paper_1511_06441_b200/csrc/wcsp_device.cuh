@@ -1,31 +1,33 @@
 // wcsp_device.cuh — device state, phase functions and kernels of the B200
 // (sm_100a) active-vertex label-correcting sweep (§4, :155-227).
 //
-// One cycle (DESIGN.md "Cycle"), c = 1, 2, ...:
+// One cycle (DESIGN.md §7), c = 1, 2, ...:
 //   sweep  : Step 1 and Step 3 (:173) — every live lane of every
 //            active vertex and every live phantom counts down by Delta; the ones
 //            reaching 0 deliver water (cand = label - f2) to their destination
 //            D with one 32-bit atomicMax on D's temporary label (Step 2,
 //            :166-168; the "temporary replacement label" of :133).  The
-//            first arrival of the cycle appends D to the triggered list (the
-//            dedupe of :164).  Survivors are compacted into the next active
-//            list / phantom pool (Steps 7-9, :207-227), block-aggregated.
-//   treat  : Steps 4, 5 and 8.1 (:176-198, :211) for every triggered Q whose
-//            temporary label beats its label (:32): an edge Q->R is triggered
-//            iff L* - f2 > max(L(R), temp(R)) (:180); if Q has no live lane
-//            (inactive, :189) the lane restarts with f1 (:190-192) and
-//            L(Q) := L*; otherwise a phantom (Q, R, L*, f1) is created
-//            (:197-198).  L* = temp(Q) (reading R23).
+//            first arrival of the cycle sets D's bit in the triggered bitmap
+//            (the dedupe of :164).  Survivors are compacted into the next
+//            active list / phantom pool (Steps 7-9, :207-227), block-aggregated.
+//   treat  : Steps 4, 5 and 8.1 (:176-198, :211) for every triggered Q, taken
+//            from the bitmap in vertex order, whose temporary label beats its
+//            label (:32): an edge Q->R is triggered iff L* - f2 >
+//            max(L(R), temp(R)) (:180); if Q has no live lane (inactive,
+//            :189) the lane restarts with f1 (:190-192) and L(Q) := L*;
+//            otherwise a phantom (Q, R, L*, f1) is created (:197-198).
+//            L* = temp(Q) (reading R23).
 //   decide : Step 6 (:204) — termination 1° (:124) / 2° (:126); Delta for the
 //            next cycle = min live residual (time skipping, :75, :95).
 // c = 0 is the initial state: A is triggered with temp M
-// and treated (reading R20).
+// and treated (reading R20).  The timing-wheel engine (wcsp_wheel.cuh) runs
+// the same treat with events instead of residual countdowns.
 //
-// Vertex state word sw[v] (u64): low u32 = label L(v) (16 bits used), high
-// u32 = temp = stamp:16 | cand:16, valid only when stamp == this cycle's.
-// Targets (B) and removed vertices carry a sentinel temp with stamp 0xFFFF
-// that an atomicMax never overwrites, so an arrival learns what D is from the
-// atomic's return value alone.
+// Vertex state word sw[v] (u64): low u32 = label L(v) (bits 0-15; bits 16-31
+// hold the wheel engine's lane-expiry time), high u32 = temp = stamp:16 |
+// cand:16, valid only when stamp == this cycle's.  Targets (B) and removed
+// vertices carry a temp sentinel with stamp 0xFFFF that an atomicMax never
+// overwrites, so an arrival learns what D is from the atomic's return value.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -33,29 +35,34 @@
 namespace wcspk {
 
 constexpr int THREADS = 256;
+constexpr int WARPS = THREADS / 32;
 constexpr int SWEEP_ITEMS = 4;           // items per thread per chunk, sweep (unrolled for MLP)
-constexpr int TREAT_ITEMS = 2;           // items per thread per chunk, treat
-constexpr int QCAP = THREADS * SWEEP_ITEMS;   // shared-memory queue capacity (overflow -> direct global append)
+constexpr int CHUNK_MAX = THREADS * SWEEP_ITEMS;
+constexpr int QP_CAP = 3072;             // shared staging of phantoms / events (overflow -> direct append)
+constexpr int QA_CAP = 2048;             // shared staging of active-list appends (never overflows)
+constexpr int WIN_WORDS = 8;             // triggered-bitmap words per warp window
+constexpr int WIN_VERTS = WIN_WORDS * 32;
 
 constexpr unsigned LBL_REMOVED = 0xFFFFu;  // label of a vertex outside G': no S6 test passes
 constexpr unsigned TMP_B = 0xFFFF0001u;    // temp sentinel of a target vertex
 constexpr unsigned TMP_REMOVED = 0xFFFF0000u;
 constexpr int ST_RUNNING = -1;
-constexpr int ST_WRAP = 100;               // stepped engine: temp stamps wrapped, host clears temps
+constexpr int ST_WRAP = 100;               // stepped engines: maintenance pass needed (host launches it)
 
 // phantom record (u64): src 30 | lane 3 | cand 16 | res 8  (cand = L* - f2(e), fixed at creation)
 constexpr int PH_LANE = 30, PH_CAND = 33, PH_RES = 49;
 constexpr unsigned STAMP_PERIOD = 65534u;  // stamps 1..0xFFFE; 0xFFFF is the sentinel
+constexpr int WHEEL = 256;                 // timing wheel buckets (f1 <= 255)
 
 struct BArr { unsigned D, cand, src, via; };   // an arrival at a target (terminating cycle only)
 
 struct Acc {                       // per-cycle accumulators, triple-buffered by cycle % 3
   unsigned n_act;                  // entries appended to the next active list
   unsigned n_pool;                 // phantoms appended to the next pool (may exceed capacity)
-  unsigned n_trig;                 // vertices appended to the triggered list (first arrivals)
+  unsigned n_trig;                 // unused (kept for layout)
   unsigned dmin;                   // min live residual after this cycle (0xFFFFFFFF = nothing live)
   unsigned long long bhit;         // max over B arrivals of (cand << 32 | ~X)
-  unsigned long long live;         // live lanes at the top of the cycle (E)
+  unsigned long long live;         // sweep: live lanes at the top of the cycle (E); wheel: lanes started
   unsigned long long arrivals, created, relabels, triggered;
   long long pend_lanes, pend_phantoms;   // timing wheel: events in flight at the top of this cycle
 };
@@ -70,7 +77,7 @@ struct View {                      // cycle state every block needs
 struct Ctl {
   View view;
   Acc acc[3];
-  unsigned long long bar;          // grid barrier arrivals (persistent engine)
+  unsigned long long bar;          // grid barrier arrivals (persistent engines)
   unsigned abort, n_barr;          // barrier watchdog fired; B-arrival list length
   long long F1, F2, X, Y;
   long long via;
@@ -79,8 +86,8 @@ struct Ctl {
   // timing-wheel engine (wcsp_wheel.cuh)
   unsigned long long ev_head;      // logical allocation head of the event ring
   unsigned wheel_overflow, pad2_;  // 2: descriptor table full
-  long long hist_t[256];           // time of cycle c (by c & 255) ...
-  unsigned long long hist_head[256];     // ... and the ring head before its treat
+  long long hist_t[WHEEL];         // time of cycle c (slot c & 255) ...
+  unsigned long long hist_head[WHEEL];   // ... and the ring head before its treat
 };
 
 struct TraceRec { long long t, delta, active_vertices, live_lanes, phantoms, triggered, arrivals, created, relabels; };
@@ -90,10 +97,11 @@ struct Dev {
   int NL;                          // lanes per vertex = 2d
   unsigned off[8];                 // lane 2k: +stride_k, lane 2k+1: -stride_k (mod 2^32)
   const void* wt;                  // weight records (f1 lane word, f2 lane word) per vertex
-  void* res;                       // lane residual words, 0 = idle lane
+  void* res;                       // sweep engine: lane residual words, 0 = idle lane
   unsigned long long* sw;          // vertex state words (label | temp)
+  unsigned* tbits;                 // triggered bitmap (first arrivals of the cycle)
+  unsigned nwords;                 // words of the bitmap
   unsigned* act[2];
-  unsigned* trig;
   unsigned long long* pool[2];
   unsigned long long pool_cap;
   BArr* barr;
@@ -112,6 +120,7 @@ struct Dev {
   unsigned* bnlane;                // [256] lane events per bucket
   unsigned dcap;
   int f1max;
+  unsigned nblocks;                // grid size of the cycle kernels (wheel region sizing)
 };
 
 template <int D> struct Tr;
@@ -177,24 +186,33 @@ template <int D> __device__ __forceinline__ typename Tr<D>::LW load_f2(const Dev
 }
 
 // ---------------------------------------------------------------------------
-// Block-local append queues (shared memory), flushed with one global atomic
-// per queue per chunk
+// Shared memory (dynamic; one layout for every kernel)
 // ---------------------------------------------------------------------------
 struct Smem {
-  unsigned q32[QCAP];              // active-vertex appends
-  unsigned qt[QCAP];               // triggered-vertex appends
-  unsigned long long qp[QCAP];     // phantom appends
-  unsigned na, nt, np;
+  unsigned long long qp[QP_CAP];   // phantom / event staging (wheel: delay in bits 56..63)
+  unsigned qa[QA_CAP];             // active-list staging
+  union {
+    unsigned wl[WARPS][WIN_VERTS]; // per-warp list of the triggered vertices of its window
+    unsigned short rank[QP_CAP];   // wheel flush: rank of an event within its delay bin
+  };
+  unsigned hist[WHEEL], hlane[WHEEL], rfill[WHEEL], rcap[WHEEL];
+  unsigned long long hbase[WHEEL], rpos[WHEEL];
+  unsigned na, np;
   unsigned base_a, base_b, flag;
   View view;
   unsigned long long bhit;
-  unsigned long long red[THREADS / 32][5];
-  unsigned redmin[THREADS / 32];
+  unsigned long long red[WARPS][5];
+  unsigned redmin[WARPS];
 };
 
+__device__ __forceinline__ Smem& smem() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return *reinterpret_cast<Smem*>(smem_raw);
+}
+
 template <class T>
-__device__ __forceinline__ void qpush(T* qbuf, unsigned* qn, bool pred, T x, unsigned* gcount, T* out,
-                                      unsigned long long cap) {
+__device__ __forceinline__ void qpush(T* qbuf, unsigned qcap, unsigned* qn, bool pred, T x, unsigned* gcount,
+                                      T* out, unsigned long long cap) {
   const unsigned m = __ballot_sync(0xFFFFFFFFu, pred);
   if (m == 0) return;
   const unsigned lane = threadIdx.x & 31u;
@@ -204,7 +222,7 @@ __device__ __forceinline__ void qpush(T* qbuf, unsigned* qn, bool pred, T x, uns
   base = __shfl_sync(0xFFFFFFFFu, base, leader);
   if (pred) {
     const unsigned idx = base + __popc(m & ((1u << lane) - 1u));
-    if (idx < (unsigned)QCAP) {
+    if (idx < qcap) {
       qbuf[idx] = x;
     } else {                        // rare: queue full, append straight to the global list
       const unsigned long long pos = atomicAdd(gcount, 1u);
@@ -213,24 +231,22 @@ __device__ __forceinline__ void qpush(T* qbuf, unsigned* qn, bool pred, T x, uns
   }
 }
 
-// Flush two queues with one reservation round (3 block barriers per chunk).
-template <class TA, class TB>
-__device__ __forceinline__ void qflush2(TA* qa, unsigned* na_s, unsigned* ga, TA* outa, unsigned long long capa,
-                                        TB* qb, unsigned* nb_s, unsigned* gb, TB* outb, unsigned long long capb,
-                                        Smem& sm) {
+// Flush the active-list and phantom queues with one reservation round.
+__device__ __forceinline__ void qflush(Smem& sm, unsigned* ga, unsigned* outa, unsigned* gp, unsigned long long* outp,
+                                       unsigned long long capp) {
   __syncthreads();
-  const unsigned na = min(*na_s, (unsigned)QCAP), nb = min(*nb_s, (unsigned)QCAP);
+  const unsigned na = min(sm.na, (unsigned)QA_CAP), np = min(sm.np, (unsigned)QP_CAP);
+  if (na == 0 && np == 0) return;                 // uniform: every thread read the same counts
   if (threadIdx.x == 0) {
     sm.base_a = na ? atomicAdd(ga, na) : 0u;
-    sm.base_b = nb ? atomicAdd(gb, nb) : 0u;
+    sm.base_b = np ? atomicAdd(gp, np) : 0u;
   }
   __syncthreads();
   const unsigned long long ba = sm.base_a, bb = sm.base_b;
-  for (unsigned i = threadIdx.x; i < na; i += THREADS)
-    if (ba + i < capa) outa[ba + i] = qa[i];
-  for (unsigned i = threadIdx.x; i < nb; i += THREADS)
-    if (bb + i < capb) outb[bb + i] = qb[i];
-  if (threadIdx.x == 0) { *na_s = 0; *nb_s = 0; }   // no push can happen before the barrier below
+  for (unsigned i = threadIdx.x; i < na; i += THREADS) outa[ba + i] = sm.qa[i];
+  for (unsigned i = threadIdx.x; i < np; i += THREADS)
+    if (bb + i < capp) outp[bb + i] = sm.qp[i];
+  if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; }  // no push can happen before the barrier below
   __syncthreads();
 }
 
@@ -248,6 +264,7 @@ __device__ __forceinline__ void block_reduce_commit(Smem& sm, unsigned dmin, uns
     a4 += __shfl_xor_sync(0xFFFFFFFFu, a4, o);
   }
   const unsigned w = threadIdx.x >> 5;
+  __syncthreads();
   if ((threadIdx.x & 31) == 0) {
     sm.redmin[w] = dmin;
     sm.red[w][0] = a0; sm.red[w][1] = a1; sm.red[w][2] = a2; sm.red[w][3] = a3; sm.red[w][4] = a4;
@@ -256,7 +273,7 @@ __device__ __forceinline__ void block_reduce_commit(Smem& sm, unsigned dmin, uns
   if (threadIdx.x == 0) {
     unsigned m = 0xFFFFFFFFu;
     unsigned long long s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
-    for (int i = 0; i < THREADS / 32; ++i) {
+    for (int i = 0; i < WARPS; ++i) {
       m = min(m, sm.redmin[i]);
       s0 += sm.red[i][0]; s1 += sm.red[i][1]; s2 += sm.red[i][2]; s3 += sm.red[i][3]; s4 += sm.red[i][4];
     }
@@ -270,15 +287,26 @@ __device__ __forceinline__ void block_reduce_commit(Smem& sm, unsigned dmin, uns
   __syncthreads();
 }
 
+// Set bit D of the triggered bitmap for every predicated lane; lanes hitting
+// the same word combine first (one atomicOr per word per warp).
+__device__ __forceinline__ void bit_set(unsigned* bits, bool pred, unsigned D) {
+  const unsigned m = __ballot_sync(0xFFFFFFFFu, pred);
+  if (m == 0 || !pred) return;
+  const unsigned word = D >> 5;
+  const unsigned peers = __match_any_sync(m, word);
+  const unsigned acc = __reduce_or_sync(peers, 1u << (D & 31u));
+  if ((threadIdx.x & 31u) == (unsigned)(__ffs(peers) - 1)) atomicOr(bits + word, acc);
+}
+
 // Water of quality `cand` reaches D from `src` (quality <= 0
 // cannot travel, :29): temp(D) := max(temp(D), cand) — one atomic whose
 // return value says whether D is a target, removed, or triggered for the
 // first time this cycle.  The comparison with L(D) ("L(S) - f2(e) > L(D)",
 // :32) is made once per triggered vertex in treat: max over all arrivals
-// beats L(D) iff max over the accepted ones does, and then they are equal.
-// Must be called by all 32 lanes of the warp (warp-aggregated queue push).
-__device__ __forceinline__ void arrive(const Dev& s, const View& v, Acc* acc, Smem& sm, bool go, unsigned D,
-                                       int cand, unsigned src, unsigned via) {
+// beats L(D) iff max over the accepted ones does, and then they are equal
+// (reading R-new-1).  Must be called by all 32 lanes of the warp.
+__device__ __forceinline__ void arrive(const Dev& s, const View& v, Acc* acc, bool go, unsigned D, int cand,
+                                       unsigned src, unsigned via) {
   go = go && cand > 0;
   bool first = false;
   if (go) {
@@ -294,11 +322,11 @@ __device__ __forceinline__ void arrive(const Dev& s, const View& v, Acc* acc, Sm
       first = os != v.stamp;
     }
   }
-  qpush<unsigned>(sm.qt, &sm.nt, first, D, &acc->n_trig, s.trig, 0xFFFFFFFFull);
+  bit_set(s.tbits, first, D);
 }
 
 // ---------------------------------------------------------------------------
-// sweep: Steps 1, 3, 7 and the retirement part of 8-9
+// sweep: Steps 1, 3, 7 and the retirement part of 8-9 (sweep engine)
 // ---------------------------------------------------------------------------
 template <int D>
 __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
@@ -340,7 +368,7 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
         if (w[it] != 0) __stcg(res + vx[it], w2);
         const bool survive = w2 != 0;
         if (survive) dmin = min(dmin, min_nonzero_byte<D, LW>(w2));
-        qpush<unsigned>(sm.q32, &sm.na, survive, vx[it], &acc->n_act, act_out, 0xFFFFFFFFull);
+        qpush<unsigned>(sm.qa, QA_CAP, &sm.na, survive, vx[it], &acc->n_act, act_out, 0xFFFFFFFFull);
       }
       unsigned lbl[SWEEP_ITEMS];
       LW f2w[SWEEP_ITEMS];
@@ -359,11 +387,9 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
           const bool fj = (fired[it] >> (8 * j + 7)) & 1;
           arr += fj;
           const int cand = (int)lbl[it] - (int)((f2w[it] >> (8 * j)) & 0xFF);
-          arrive(s, v, acc, sm, fj, vx[it] + s.off[j], cand, vx[it], 0u);
+          arrive(s, v, acc, fj, vx[it] + s.off[j], cand, vx[it], 0u);
         }
       }
-      qflush2<unsigned, unsigned>(sm.q32, &sm.na, &acc->n_act, act_out, 0xFFFFFFFFull, sm.qt, &sm.nt,
-                                  &acc->n_trig, s.trig, 0xFFFFFFFFull, sm);
     } else {
       const unsigned pc = ch - na_ch;
       unsigned long long p[SWEEP_ITEMS];
@@ -379,107 +405,191 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
         const bool keep = r > v.delta;
         if (keep) dmin = min(dmin, r - v.delta);
         arr += fire;
-        qpush<unsigned long long>(sm.qp, &sm.np, keep, p[it] - ((unsigned long long)v.delta << PH_RES),
+        qpush<unsigned long long>(sm.qp, QP_CAP, &sm.np, keep, p[it] - ((unsigned long long)v.delta << PH_RES),
                                   &acc->n_pool, pool_out, s.pool_cap);
         const unsigned src = (unsigned)p[it] & 0x3FFFFFFFu;
         const unsigned lane = (unsigned)(p[it] >> PH_LANE) & 7u;
         const int cand = (int)((p[it] >> PH_CAND) & 0xFFFFu);
-        arrive(s, v, acc, sm, fire, src + s.off[lane], cand, src, 1u);
+        arrive(s, v, acc, fire, src + s.off[lane], cand, src, 1u);
       }
-      qflush2<unsigned long long, unsigned>(sm.qp, &sm.np, &acc->n_pool, pool_out, s.pool_cap, sm.qt, &sm.nt,
-                                            &acc->n_trig, s.trig, 0xFFFFFFFFull, sm);
     }
+    qflush(sm, &acc->n_act, act_out, &acc->n_pool, pool_out, s.pool_cap);
   }
   block_reduce_commit(sm, dmin, live, arr, 0, 0, 0, acc);
 }
 
 // ---------------------------------------------------------------------------
-// treat: Steps 4, 5, 8.1 (+ the activation half of 8.2 / 9)
+// Triggered-bitmap windows: warp w of the block takes window
+// (round * gridDim + block) * WARPS + w, clears it and lists its set bits in
+// ascending vertex order (sorted processing: neighbouring Q share sectors).
 // ---------------------------------------------------------------------------
-template <int D>
-__device__ void phase_treat(const Dev& s, const View& v, Smem& sm, unsigned n_trig) {
-  using LW = typename Tr<D>::LW;
-  Acc* acc = &s.ctl->acc[v.c % 3];
-  LW* res = reinterpret_cast<LW*>(s.res);
-  unsigned* act_out = s.act[v.cur ^ 1];
-  unsigned long long* pool_out = s.pool[v.cur ^ 1];
-  const unsigned items = n_trig >= 2u * THREADS * gridDim.x ? 2u : 1u;
-  const unsigned chunk = items * THREADS;
-  const unsigned nch = (n_trig + chunk - 1) / chunk;
-  unsigned dmin = 0xFFFFFFFFu;
-  unsigned long long created = 0, relabels = 0, triggered = 0;
-
-  for (unsigned ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-    unsigned q[TREAT_ITEMS];
-#pragma unroll
-    for (int it = 0; it < TREAT_ITEMS; ++it) {
-      const unsigned i = ch * chunk + it * THREADS + threadIdx.x;
-      q[it] = ((unsigned)it < items && i < n_trig) ? __ldcg(s.trig + i) : 0xFFFFFFFFu;
-    }
-    unsigned long long swq[TREAT_ITEMS];
-    LW w[TREAT_ITEMS];
-    WRec<LW> wr[TREAT_ITEMS];
-#pragma unroll
-    for (int it = 0; it < TREAT_ITEMS; ++it) {
-      const bool valid = q[it] != 0xFFFFFFFFu;
-      swq[it] = valid ? __ldcg(s.sw + q[it]) : 0ull;
-      w[it] = valid ? __ldcg(res + q[it]) : (LW)0;
-      wr[it] = valid ? load_wt<D>(s, q[it]) : WRec<LW>{0, 0};
-    }
-#pragma unroll
-    for (int it = 0; it < TREAT_ITEMS; ++it) {
-      const int lq = (int)(swq[it] & 0xFFFFu);
-      const int lstar = (int)((swq[it] >> 32) & 0xFFFFu);         // L* = temp(Q) (reading R23)
-      const bool trig = q[it] != 0xFFFFFFFFu && lstar > lq;       // the water improves Q
-      const bool inactive = trig && w[it] == 0;                   // no live lane after the decrement (R6)
-      triggered += trig;
-      unsigned long long swr[2 * D];
-#pragma unroll
-      for (int j = 0; j < 2 * D; ++j) {
-        const unsigned f1j = (unsigned)(wr[it].f1 >> (8 * j)) & 0xFFu;
-        const unsigned f2j = s.minf ? 0u : (unsigned)(wr[it].f2 >> (8 * j)) & 0xFFu;
-        const bool test = trig && f1j != 0 && lstar - (int)f2j > 0;
-        swr[j] = test ? __ldcg(s.sw + (q[it] + s.off[j])) : 0xFFFFull;   // untested lanes read as "removed"
-      }
-      LW neww = 0;
-#pragma unroll
-      for (int j = 0; j < 2 * D; ++j) {
-        const unsigned f1j = (unsigned)(wr[it].f1 >> (8 * j)) & 0xFFu;
-        const unsigned f2j = s.minf ? 0u : (unsigned)(wr[it].f2 >> (8 * j)) & 0xFFu;
-        const int c = lstar - (int)f2j;
-        const unsigned rl = (unsigned)swr[j] & 0xFFFFu;
-        const unsigned rtw = (unsigned)(swr[j] >> 32);
-        const unsigned rt = (rtw >> 16) == v.stamp ? (rtw & 0xFFFFu) : 0u;
-        const bool pass = c > (int)max(rl, rt);                   // edge triggered
-        if (pass) dmin = min(dmin, f1j);
-        if (pass && inactive) neww |= (LW)f1j << (8 * j);         // activate, time restored to f1 (:192)
-        const bool ph = pass && !inactive;                        // phantom (Q, R, L*, f1) (:197-198)
-        created += ph;
-        const unsigned long long prec = (unsigned long long)q[it] | ((unsigned long long)j << PH_LANE) |
-                                        ((unsigned long long)(unsigned)c << PH_CAND) |
-                                        ((unsigned long long)f1j << PH_RES);
-        qpush<unsigned long long>(sm.qp, &sm.np, ph, prec, &acc->n_pool, pool_out, s.pool_cap);
-      }
-      if (inactive) {                                             // Step 8.1
-        *lbl_ptr(s.sw, q[it]) = (unsigned)lstar;
-        relabels += 1;
-        if (neww) __stcg(res + q[it], neww);
-      }
-      qpush<unsigned>(sm.q32, &sm.na, inactive && neww != 0, q[it], &acc->n_act, act_out, 0xFFFFFFFFull);
-    }
-    qflush2<unsigned, unsigned long long>(sm.q32, &sm.na, &acc->n_act, act_out, 0xFFFFFFFFull, sm.qp, &sm.np,
-                                          &acc->n_pool, pool_out, s.pool_cap, sm);
+__device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsigned* list) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned wi = win * WIN_WORDS + lane;
+  unsigned w = 0;
+  if (lane < (unsigned)WIN_WORDS && wi < s.nwords) {
+    w = __ldcg(s.tbits + wi);
+    if (w) s.tbits[wi] = 0u;
   }
-  block_reduce_commit(sm, dmin, 0, 0, created, relabels, triggered, acc);
+  const unsigned c = __popc(w);
+  unsigned x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if ((int)lane >= o) x += y;
+  }
+  const unsigned total = __shfl_sync(0xFFFFFFFFu, x, 31);
+  unsigned pos = x - c;
+  while (w) {
+    list[pos++] = wi * 32u + (unsigned)(__ffs(w) - 1);
+    w &= w - 1u;
+  }
+  __syncwarp();
+  return total;
 }
 
 // ---------------------------------------------------------------------------
-// decide: Step 6 + time skipping.  Executed by one thread; writes ctl if writer.
+// treat: Steps 4, 5, 8.1 for one triggered vertex q (both engines).
+// WHEEL = false: lanes are residual bytes in res[q]; phantoms go to the pool.
+// WHEEL = true : lanes and phantoms are events filed at t + f1 (wcsp_wheel.cuh).
+// ---------------------------------------------------------------------------
+template <int D, bool WHEEL_ENGINE>
+__device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
+                                          unsigned& dmin, unsigned long long& created,
+                                          unsigned long long& relabels, unsigned long long& triggered,
+                                          unsigned long long& lanes_started);
+
+__device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
+  return ((texp16 - (unsigned)t) & 0xFFFFu) - 1u < 255u;   // texp in (t, t + 255]
+}
+
+// Stage one event for the wheel (defined in wcsp_wheel.cuh).
+__device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t);
+
+template <int D, bool WHEEL_ENGINE>
+__device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
+                                          unsigned& dmin, unsigned long long& created,
+                                          unsigned long long& relabels, unsigned long long& triggered,
+                                          unsigned long long& lanes_started) {
+  using LW = typename Tr<D>::LW;
+  const bool valid = q != 0xFFFFFFFFu;
+  const unsigned long long swq = valid ? __ldcg(s.sw + q) : 0ull;
+  const WRec<LW> wr = valid ? load_wt<D>(s, q) : WRec<LW>{0, 0};
+  LW w = 0;
+  if constexpr (!WHEEL_ENGINE) w = valid ? __ldcg(reinterpret_cast<LW*>(s.res) + q) : (LW)0;
+  const int lq = (int)(swq & 0xFFFFu);
+  const int lstar = (int)((swq >> 32) & 0xFFFFu);                 // L* = temp(Q) (reading R23)
+  const bool trig = valid && lstar > lq;                          // the water improves Q
+  bool inactive;
+  if constexpr (WHEEL_ENGINE) inactive = trig && !lane_live((unsigned)(swq >> 16) & 0xFFFFu, v.t);
+  else inactive = trig && w == 0;                                 // no live lane after the decrement (R6)
+  triggered += trig;
+  unsigned long long swr[2 * D];
+#pragma unroll
+  for (int j = 0; j < 2 * D; ++j) {
+    const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
+    const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
+    const bool test = trig && f1j != 0 && lstar - (int)f2j > 0;
+    swr[j] = test ? __ldcg(s.sw + (q + s.off[j])) : 0xFFFFull;    // untested lanes read as "removed"
+  }
+  LW neww = 0;
+  unsigned fmax = 0;
+#pragma unroll
+  for (int j = 0; j < 2 * D; ++j) {
+    const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
+    const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
+    const int c = lstar - (int)f2j;
+    const unsigned rl = (unsigned)swr[j] & 0xFFFFu;
+    const unsigned rtw = (unsigned)(swr[j] >> 32);
+    const unsigned rt = (rtw >> 16) == v.stamp ? (rtw & 0xFFFFu) : 0u;
+    const bool pass = c > (int)max(rl, rt);                       // edge triggered
+    const bool ph = pass && !inactive;                            // phantom (Q, R, L*, f1) (:197-198)
+    created += ph;
+    lanes_started += pass && inactive;                            // activate, time restored to f1 (:192)
+    if constexpr (WHEEL_ENGINE) {
+      if (pass && inactive) fmax = max(fmax, f1j);
+      const unsigned long long rec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
+                                     ((unsigned long long)(unsigned)c << PH_CAND) |
+                                     ((unsigned long long)(inactive ? 1u : 0u) << 49);
+      ev_push(s, sm, pass, rec, f1j, v.t);
+    } else {
+      if (pass) dmin = min(dmin, f1j);
+      if (pass && inactive) neww |= (LW)f1j << (8 * j);
+      const unsigned long long prec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
+                                      ((unsigned long long)(unsigned)c << PH_CAND) |
+                                      ((unsigned long long)f1j << PH_RES);
+      qpush<unsigned long long>(sm.qp, QP_CAP, &sm.np, ph, prec, &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
+    }
+  }
+  if (inactive) {                                                 // Step 8.1
+    relabels += 1;
+    if constexpr (WHEEL_ENGINE) {
+      const unsigned nt = (unsigned)((fmax ? v.t + fmax : v.t) & 0xFFFF);
+      *lbl_ptr(s.sw, q) = (unsigned)lstar | (nt << 16);
+    } else {
+      *lbl_ptr(s.sw, q) = (unsigned)lstar;
+      if (neww) __stcg(reinterpret_cast<LW*>(s.res) + q, neww);
+    }
+  }
+  if constexpr (!WHEEL_ENGINE)
+    qpush<unsigned>(sm.qa, QA_CAP, &sm.na, inactive && neww != 0, q, &acc->n_act, s.act[v.cur ^ 1], 0xFFFFFFFFull);
+}
+
+// Flush hook of the wheel (defined in wcsp_wheel.cuh).
+__device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, bool final_flush);
+
+template <int D, bool WHEEL_ENGINE>
+__device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
+  Acc* acc = &s.ctl->acc[v.c % 3];
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const unsigned nwin = (s.nwords + WIN_WORDS - 1) / WIN_WORDS;
+  const unsigned per_round = gridDim.x * WARPS;
+  unsigned dmin = 0xFFFFFFFFu;
+  unsigned long long created = 0, relabels = 0, triggered = 0, lanes_started = 0;
+  if constexpr (WHEEL_ENGINE) {
+    for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.rcap[d] = 0; sm.rfill[d] = 0; }
+    __syncthreads();
+  }
+  for (unsigned r0 = 0; r0 < nwin; r0 += per_round) {
+    const unsigned win = r0 + blockIdx.x * WARPS + warp;
+    const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
+    for (unsigned b = 0; b < total; b += 32) {
+      const unsigned q = b + lane < total ? sm.wl[warp][b + lane] : 0xFFFFFFFFu;
+      treat_one<D, WHEEL_ENGINE>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started);
+    }
+    if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, false);
+    else qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
+  }
+  if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, true);
+  // wheel: lanes started ride in the 'live' slot (the sweep counts live lanes there in its sweep)
+  block_reduce_commit(sm, dmin, WHEEL_ENGINE ? lanes_started : 0ull, 0, created, relabels, triggered, acc);
+}
+
+// ---------------------------------------------------------------------------
+// decide (sweep engine): Step 6 + time skipping.  One thread; writes ctl if writer.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void reset_acc(Acc* a) {
   a->n_act = 0; a->n_pool = 0; a->n_trig = 0; a->dmin = 0xFFFFFFFFu;
   a->bhit = 0; a->live = 0; a->arrivals = 0; a->created = 0; a->relabels = 0; a->triggered = 0;
   a->pend_lanes = 0; a->pend_phantoms = 0;
+}
+
+__device__ __forceinline__ void resolve_hit(const Dev& s, unsigned long long bhit, long long t) {
+  Ctl* C = s.ctl;
+  const unsigned q = (unsigned)(bhit >> 32);
+  const unsigned X = 0xFFFFFFFFu - (unsigned)bhit;
+  // Y = smallest source among the arrivals at X carrying q; a regular edge wins over a phantom (R5)
+  const unsigned nb = min(__ldcg(&C->n_barr), s.barr_cap);
+  unsigned long long best = ~0ull;
+  for (unsigned k = 0; k < nb; ++k) {
+    const BArr b = s.barr[k];
+    if (b.D == X && b.cand == q) best = min(best, ((unsigned long long)b.src << 1) | b.via);
+  }
+  C->F1 = t;
+  C->F2 = s.minf ? -1 : (long long)s.M - q;
+  C->X = X;
+  C->Y = (long long)(best >> 1);
+  C->via = (long long)(best & 1);
 }
 
 __device__ void decide(const Dev& s, View& v, bool writer) {
@@ -505,22 +615,7 @@ __device__ void decide(const Dev& s, View& v, bool writer) {
   }
   if (bhit) {
     nv.status = 0;  // WCSP_REACHED
-    if (writer) {
-      const unsigned q = (unsigned)(bhit >> 32);
-      const unsigned X = 0xFFFFFFFFu - (unsigned)bhit;
-      // Y = smallest source among the arrivals at X carrying q; a regular edge wins over a phantom
-      const unsigned nb = min(__ldcg(&C->n_barr), s.barr_cap);
-      unsigned long long best = ~0ull;
-      for (unsigned k = 0; k < nb; ++k) {
-        const BArr b = s.barr[k];
-        if (b.D == X && b.cand == q) best = min(best, ((unsigned long long)b.src << 1) | b.via);
-      }
-      C->F1 = v.t;
-      C->F2 = s.minf ? -1 : (long long)s.M - q;
-      C->X = X;
-      C->Y = (long long)(best >> 1);
-      C->via = (long long)(best & 1);
-    }
+    if (writer) resolve_hit(s, bhit, v.t);
   } else if (n_pool > s.pool_cap) {
     nv.status = 8;  // WCSP_EOVERFLOW
     if (writer) C->need_pool = n_pool;
@@ -546,7 +641,7 @@ __device__ void decide(const Dev& s, View& v, bool writer) {
 }
 
 // ---------------------------------------------------------------------------
-// grid barrier for the cooperative persistent kernel (monotone counter)
+// grid barrier for the cooperative persistent kernels (monotone counter)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -598,7 +693,7 @@ __device__ __forceinline__ void load_view(const Dev& s, Smem& sm, View& v) {
 }
 
 __device__ __forceinline__ void init_smem(Smem& sm) {
-  if (threadIdx.x == 0) { sm.na = 0; sm.nt = 0; sm.np = 0; }
+  if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; }
   __syncthreads();
 }
 
@@ -613,11 +708,11 @@ __device__ __forceinline__ void clear_temps(const Dev& s) {
 }
 
 // ---------------------------------------------------------------------------
-// kernels
+// kernels (sweep engine)
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(THREADS, 4) k_persistent(Dev s) {
-  __shared__ Smem sm;
+  Smem& sm = smem();
   init_smem(sm);
   View v;
   load_view(s, sm, v);
@@ -630,16 +725,12 @@ __global__ void __launch_bounds__(THREADS, 4) k_persistent(Dev s) {
       target += G;
       if (!grid_sync(s.ctl, target, sm)) return;
     }
-    if (threadIdx.x == 0) {
-      sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
-      sm.base_a = __ldcg(&s.ctl->acc[v.c % 3].n_trig);
-    }
+    if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
     __syncthreads();
     const unsigned long long bhit = sm.bhit;
-    const unsigned n_trig = sm.base_a;
     __syncthreads();
     if (!bhit) {                                   // S5 precedes S6: the final cycle skips the treat
-      phase_treat<D>(s, v, sm, n_trig);
+      phase_treat<D, false>(s, v, sm);
       target += G;
       if (!grid_sync(s.ctl, target, sm)) return;
     }
@@ -660,8 +751,8 @@ __global__ void __launch_bounds__(THREADS, 4) k_persistent(Dev s) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS) k_sweep(Dev s) {
-  __shared__ Smem sm;
+__global__ void __launch_bounds__(THREADS, 4) k_sweep(Dev s) {
+  Smem& sm = smem();
   init_smem(sm);
   View v;
   load_view(s, sm, v);
@@ -672,14 +763,13 @@ __global__ void __launch_bounds__(THREADS) k_sweep(Dev s) {
 
 template <int D>
 __global__ void __launch_bounds__(THREADS, 4) k_treat(Dev s) {
-  __shared__ Smem sm;
+  Smem& sm = smem();
   init_smem(sm);
   View v;
   load_view(s, sm, v);
   if (v.status != ST_RUNNING) return;
-  const Acc* a = &s.ctl->acc[v.c % 3];
-  if (__ldcg(&a->bhit)) return;
-  phase_treat<D>(s, v, sm, __ldcg(&a->n_trig));
+  if (__ldcg(&s.ctl->acc[v.c % 3].bhit)) return;
+  phase_treat<D, false>(s, v, sm);
 }
 
 __global__ void k_decide(Dev s) {
@@ -692,39 +782,36 @@ __global__ void k_decide(Dev s) {
 
 __global__ void __launch_bounds__(THREADS) k_clear_temps(Dev s) { clear_temps(s); }
 
-// Initial state (reading R20): L = M on A, 0 elsewhere,
-// target / removed sentinels, no live lane, A triggered with temp M.
+// Initial state (reading R20): L = 0 everywhere, target /
+// removed sentinels, no live lane, A triggered with temp M (the treat of
+// c = 0 then sets L = M on A and starts its lanes).
 __global__ void __launch_bounds__(THREADS) k_init(Dev s, const uint8_t* maskA, const uint8_t* maskB,
                                                   const uint8_t* present, int lblA, int d) {
-  Acc* acc = &s.ctl->acc[0];
   const unsigned N = s.N;
-  for (unsigned long long base = (unsigned long long)blockIdx.x * THREADS; base < N;
-       base += (unsigned long long)gridDim.x * THREADS) {
-    const unsigned long long i = base + threadIdx.x;
-    const bool valid = i < N;
-    bool a = false;
-    if (valid) {
-      const bool p = present ? present[i] != 0 : true;
-      a = p && maskA[i];
-      const bool b = p && maskB[i];
-      unsigned lbl = 0, tmp = 0;
-      if (!p) { lbl = LBL_REMOVED; tmp = TMP_REMOVED; }
-      else if (b) { lbl = 0; tmp = TMP_B; }
-      else if (a) { lbl = 0; tmp = (stamp_of(0) << 16) | (unsigned)lblA; }   // treat(c = 0) sets L = M
-      s.sw[i] = ((unsigned long long)tmp << 32) | lbl;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * THREADS + threadIdx.x; i < N;
+       i += (unsigned long long)gridDim.x * THREADS) {
+    const bool p = present ? present[i] != 0 : true;
+    const bool a = p && maskA[i];
+    const bool b = p && maskB[i];
+    unsigned lbl = 0, tmp = 0;
+    if (!p) { lbl = LBL_REMOVED; tmp = TMP_REMOVED; }
+    else if (b) { lbl = 0; tmp = TMP_B; }
+    else if (a) { lbl = 0; tmp = (stamp_of(0) << 16) | (unsigned)lblA; }
+    s.sw[i] = ((unsigned long long)tmp << 32) | lbl;
+    if (s.res) {
       if (d <= 2) reinterpret_cast<uint32_t*>(s.res)[i] = 0u;
       else reinterpret_cast<unsigned long long*>(s.res)[i] = 0ull;
     }
-    // direct global append (order irrelevant); warp-aggregated
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, a);
-    if (m) {
-      const unsigned lane = threadIdx.x & 31u;
-      const int leader = __ffs(m) - 1;
-      unsigned b = 0;
-      if ((int)lane == leader) b = atomicAdd(&acc->n_trig, (unsigned)__popc(m));
-      b = __shfl_sync(0xFFFFFFFFu, b, leader);
-      if (a) s.trig[b + __popc(m & ((1u << lane) - 1u))] = (unsigned)i;
+  }
+  // triggered bitmap = A
+  for (unsigned long long w = (unsigned long long)blockIdx.x * THREADS + threadIdx.x; w < s.nwords;
+       w += (unsigned long long)gridDim.x * THREADS) {
+    unsigned bits = 0;
+    for (unsigned b = 0; b < 32; ++b) {
+      const unsigned long long i = w * 32 + b;
+      if (i < N && maskA[i] && (present ? present[i] != 0 : true) && !maskB[i]) bits |= 1u << b;
     }
+    s.tbits[w] = bits;
   }
 }
 
@@ -765,7 +852,8 @@ __global__ void __launch_bounds__(THREADS) k_weights(Dev s, const uint8_t* f1, c
   }
 }
 
-// Validation counters (wcsp.h rules): [0] |A|, [1] |B|, [2] |A n B|, [3] present edges with f2 = 0.
+// Validation counters (wcsp.h rules): [0] |A|, [1] |B|, [2] |A n B|, [3] present edges with f2 = 0,
+// [4] max f1 over present edges.
 __global__ void __launch_bounds__(THREADS) k_validate(unsigned long long N, int d, long long n0, long long n1,
                                                       long long n2, long long n3, const uint8_t* f1,
                                                       const uint8_t* f2, const uint8_t* maskA,
@@ -773,6 +861,7 @@ __global__ void __launch_bounds__(THREADS) k_validate(unsigned long long N, int 
                                                       unsigned long long* out) {
   const long long n[4] = {n0, n1, n2, n3};
   unsigned long long c[4] = {0, 0, 0, 0};
+  unsigned fmax = 0;
   for (unsigned long long v = (unsigned long long)blockIdx.x * THREADS + threadIdx.x; v < N;
        v += (unsigned long long)gridDim.x * THREADS) {
     const bool p = present ? present[v] != 0 : true;
@@ -781,12 +870,16 @@ __global__ void __launch_bounds__(THREADS) k_validate(unsigned long long N, int 
     unsigned long long stride = 1;
     for (int k = 0; k < d; ++k) {
       const unsigned long long xk = (v / stride) % (unsigned long long)n[k];
-      if (xk + 1 < (unsigned long long)n[k]) c[3] += (f1[k * N + v] != 0 && f2[k * N + v] == 0);
+      if (xk + 1 < (unsigned long long)n[k]) {
+        c[3] += (f1[k * N + v] != 0 && f2[k * N + v] == 0);
+        fmax = max(fmax, (unsigned)f1[k * N + v]);
+      }
       stride *= (unsigned long long)n[k];
     }
   }
   for (int i = 0; i < 4; ++i)
     if (c[i]) atomicAdd(out + i, c[i]);
+  if (fmax) atomicMax(out + 4, (unsigned long long)fmax);
 }
 
 }  // namespace wcspk

@@ -24,7 +24,8 @@ M_MAX = 65533
 REACHED, INFEASIBLE, EINVAL, EMISMATCH, EBUDGET, ENOMEM, ECUDA, ENCCL, EOVERFLOW = range(9)
 MEM_HOST, MEM_DEVICE = 0, 1
 JUMP, UNIT = 0, 1
-PERSISTENT, STEPPED = 0, 1
+PERSISTENT, STEPPED, WHEEL, WHEEL_STEPPED = 0, 1, 2, 3
+ENGINES = {"persistent": PERSISTENT, "stepped": STEPPED, "wheel": WHEEL, "wheel_stepped": WHEEL_STEPPED}
 _STATUS = {0: "REACHED", 1: "INFEASIBLE", 2: "EINVAL", 3: "EMISMATCH", 4: "EBUDGET", 5: "ENOMEM",
            6: "ECUDA", 7: "ENCCL", 8: "EOVERFLOW"}
 
@@ -194,7 +195,7 @@ class Solver:
         self.N = int(np.prod(self.shape))
         o = _Options()
         o.time_mode = {"jump": JUMP, "unit": UNIT}[time_mode]
-        o.engine = {"persistent": PERSISTENT, "stepped": STEPPED}[engine]
+        o.engine = ENGINES[engine]
         o.demote_twin = 0
         o.device = int(device)
         o.cycle_budget = int(cycle_budget)

@@ -18,7 +18,7 @@ from paper_1511_06441_b200 import wcsp
 pytestmark = pytest.mark.gpu
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fixtures.json")))
-ENGINES = ["persistent", "stepped"]
+ENGINES = ["persistent", "stepped", "wheel", "wheel_stepped"]
 
 
 def check(inst, engine="persistent", time_mode="jump", counters=True, want=None):
@@ -114,6 +114,34 @@ def test_C1_infeasible_and_C1b(seed):
     assert r.status == wcsp.INFEASIBLE
     check(c)
     check(I.config_C1(seed, 65))
+
+
+def test_wheel_equals_sweep_counters():
+    """The timing wheel is an exact reformulation of Steps 1/3/7:
+    same outputs and the same work counters as the residual-countdown sweep."""
+    rng = np.random.default_rng(606)
+    insts = [I.random_small(rng, shapes=[(12, 12), (6, 6, 6), (30, 9), (3, 4, 3, 3)], M_range=(5, 120),
+                            max_sources=5, max_targets=5, hole_prob=0.1) for _ in range(60)]
+    insts += [I.config_face((96, 96), 1, 400), I.config_face((24, 24, 24), 2, 150), I.fixture_B(), I.fixture_D(),
+              I.speedway_instance(20)]
+    for inst in insts:
+        rs = wcsp.solve(inst, engine="persistent")
+        for e in ("wheel", "wheel_stepped"):
+            rw = wcsp.solve(inst, engine=e)
+            assert rw.key() == rs.key(), (inst.name, e)
+            assert (rw.cycles, rw.edge_updates, rw.arrivals, rw.phantoms_created, rw.relabels, rw.triggered) == \
+                   (rs.cycles, rs.edge_updates, rs.arrivals, rs.phantoms_created, rs.relabels, rs.triggered), \
+                   (inst.name, e, rw, rs)
+    # per-cycle E and P agree too
+    inst = I.config_face((64, 64), 3, 260)
+    with wcsp.Solver(inst, trace_cap=4096) as s:
+        s.solve()
+        ts = s.trace()
+    with wcsp.Solver(inst, engine="wheel", trace_cap=4096) as s:
+        s.solve()
+        tw = s.trace()
+    for k in ("t", "live_lanes", "phantoms", "triggered", "arrivals", "created", "relabels"):
+        assert np.array_equal(ts[k], tw[k]), k
 
 
 def test_determinism_repeated_runs():

@@ -57,11 +57,19 @@ def workload_instance(name: str, seed: int):
     return I.config_face(WORKLOADS[name]["shape"], seed, M, name=name), table[key]
 
 
-def alg_bytes(r, d: int) -> int:
-    """Algorithmic bytes the method must move (SURVEY §8(d) 'alg', DESIGN.md
-    "Roofline"): 2 B per live lane/phantom per cycle (u8 residual read+write),
-    13 B per arrival, (2d*8 + 22) B per triggered vertex, 8 B per phantom
-    created, 2 B per relabel."""
+def alg_bytes(r, d: int, engine: str) -> int:
+    """Algorithmic bytes per solve.
+    sweep engines (SURVEY §8(d) 'alg'): 2 B per live lane/phantom per cycle
+      (u8 residual read + write), 13 B per arrival, (2d*8 + 22) B per triggered
+      vertex, 8 B per phantom created, 2 B per relabel.
+    wheel engines (events are not touched between creation and arrival):
+      8 B written per event created (lanes started + phantoms), 8 B read +
+      8 B temp read-modify-write per arrival, (8 + 16 + 2d*8) B per triggered
+      vertex (its state word, weight record, neighbours' state words), 4 B per
+      relabel."""
+    if engine.startswith("wheel"):
+        return (8 * (r.lanes_started + r.phantoms_created) + 16 * r.arrivals + (24 + 2 * d * 8) * r.triggered
+                + 4 * r.relabels)
     return (2 * r.edge_updates + 13 * r.arrivals + (2 * d * 8 + 22) * r.triggered + 8 * r.phantoms_created
             + 2 * r.relabels)
 
@@ -167,7 +175,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
-    ap.add_argument("--engine", default="persistent", choices=["persistent", "stepped", "wheel", "wheel_stepped"])
+    ap.add_argument("--engine", default="wheel", choices=["persistent", "stepped", "wheel", "wheel_stepped"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -224,7 +232,7 @@ def main():
     # roofline of the dominant kernel (the cycle kernel; one launch per solve)
     r0 = results[0]
     cyc_ms = statistics.mean(r.cycle_ms for r in results)
-    ab = alg_bytes(r0, d)
+    ab = alg_bytes(r0, d, args.engine)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)

@@ -113,8 +113,9 @@ typedef struct {
   int64_t triggered;        /* sum over cycles of triggered vertices */
   int64_t phantoms_created;
   int64_t relabels;
-  int64_t peak_active;      /* max active-vertex list size */
-  int64_t peak_phantoms;    /* max live phantoms */
+  int64_t lanes_started;    /* active edges (re)started by inactive triggered vertices */
+  int64_t peak_active;      /* max active-vertex list size (sweep engines) */
+  int64_t peak_phantoms;    /* sweep: max live phantoms; wheel: max live edges + phantoms */
   int64_t phantom_capacity; /* pool capacity used by the successful run */
   int64_t kernel_launches;  /* CUDA kernels this solve launched */
   double device_ms;         /* device time of the solve (init + cycles), CUDA events */
@@ -131,6 +132,9 @@ typedef struct {
   int64_t arrivals;         /* R */
   int64_t created;          /* phantoms created */
   int64_t relabels;
+  int64_t tested;           /* triggered-bitmap entries examined by the treat phase */
+  int64_t ns_arrive;        /* device ns of the arrival phase (sweep / fire) incl. its grid barrier */
+  int64_t ns_treat;         /* device ns of the treat phase incl. its grid barrier */
 } wcsp_trace_rec;
 
 typedef struct wcsp_handle wcsp_handle;

@@ -13,7 +13,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libwcsp.so")
 SOURCES = [os.path.join(CSRC, "wcsp.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "wcsp_device.cuh"), os.path.join(ROOT, "include", "wcsp.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + [
+    os.path.join(ROOT, "include", "wcsp.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -67,7 +68,7 @@ struct wcsp_handle {
   unsigned long long* ev = nullptr;                  // wheel engines only
   unsigned long long ev_cap = 0;
   unsigned long long* bdesc = nullptr;
-  unsigned* bcounts = nullptr;                       // bndesc | bnev | bnlane (3 x 256)
+  unsigned* bcounts = nullptr;                       // bnev [256] | bnlane [256] | bndesc [256][grid]
   unsigned dcap = 0;
   int f1max = 255;
   Ctl* ctl = nullptr;
@@ -145,9 +146,9 @@ Dev make_dev(const wcsp_handle* h) {
   s.ev = h->ev;
   s.ev_mask = h->ev_cap ? h->ev_cap - 1 : 0;
   s.bdesc = h->bdesc;
-  s.bndesc = h->bcounts;
-  s.bnev = h->bcounts ? h->bcounts + WHEEL : nullptr;
-  s.bnlane = h->bcounts ? h->bcounts + 2 * WHEEL : nullptr;
+  s.bnev = h->bcounts;
+  s.bnlane = h->bcounts ? h->bcounts + WHEEL : nullptr;
+  s.bndesc = h->bcounts ? h->bcounts + 2 * WHEEL : nullptr;
   s.dcap = h->dcap;
   s.f1max = h->f1max;
   s.nblocks = (unsigned)h->grid;
@@ -185,7 +186,7 @@ wcsp_status alloc_desc(wcsp_handle* h, unsigned dcap) {
   if (h->bdesc) cudaFree(h->bdesc);
   h->bdesc = nullptr;
   h->dcap = 0;
-  CK(cudaMalloc(&h->bdesc, (size_t)WHEEL * dcap * sizeof(unsigned long long)));
+  CK(cudaMalloc(&h->bdesc, (size_t)WHEEL * h->grid * dcap * sizeof(unsigned long long)));
   h->dcap = dcap;
   return WCSP_REACHED;
 }
@@ -284,6 +285,36 @@ void release(wcsp_handle* h) {
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
 }
 
+// Keep the vertex state words (the atomics' targets and the neighbour tests'
+// reads) resident in L2: an access-policy window on the solver's stream marks
+// up to the device's persisting set-aside as evict-last; streaming traffic
+// (events, weight records) uses evict-first hints in the kernels.  Disabled
+// with WCSP_L2_PERSIST=0.
+void set_l2_window(wcsp_handle* h) {
+  const char* env = getenv("WCSP_L2_PERSIST");
+  if (env && env[0] == '0') return;
+  int max_persist = 0, max_window = 0;
+  if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->dev) != cudaSuccess ||
+      max_persist <= 0 || max_window <= 0) {
+    cudaGetLastError();
+    return;
+  }
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const size_t bytes = std::min<size_t>((size_t)h->N * sizeof(unsigned long long), (size_t)max_window);
+  cudaStreamAttrValue attr{};
+  attr.accessPolicyWindow.base_ptr = h->sw;
+  attr.accessPolicyWindow.num_bytes = bytes;
+  attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)bytes);
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  if (cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
+    cudaGetLastError();
+}
+
 wcsp_status reset_ctl(wcsp_handle* h) {
   memset(h->h_ctl, 0, sizeof(Ctl));
   Ctl& c = *h->h_ctl;
@@ -292,7 +323,8 @@ wcsp_status reset_ctl(wcsp_handle* h) {
   c.view.region = 256;
   for (int i = 0; i < 3; ++i) c.acc[i].dmin = 0xFFFFFFFFu;
   CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
-  if (is_wheel(h->opt.engine)) CK(cudaMemsetAsync(h->bcounts, 0, 3 * WHEEL * sizeof(unsigned), h->stream));
+  if (is_wheel(h->opt.engine))
+    CK(cudaMemsetAsync(h->bcounts, 0, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned), h->stream));
   return WCSP_REACHED;
 }
 
@@ -404,6 +436,7 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   r->triggered = c.triggered;
   r->phantoms_created = c.created;
   r->relabels = c.relabels;
+  r->lanes_started = c.started;
   r->peak_active = c.peak_active;
   r->peak_phantoms = c.peak_phantoms;
   r->phantom_capacity = (long long)(is_wheel(h->opt.engine) ? h->ev_cap : h->pool_cap);
@@ -522,15 +555,16 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
   const unsigned long long cap = opt.phantom_capacity > 0 ? (unsigned long long)opt.phantom_capacity
                                                           : std::max<unsigned long long>(4 * N, 1ull << 20);
   if (is_wheel(opt.engine)) {
-    CKH(alloc_ring(h, std::max<unsigned long long>(cap, (unsigned long long)h->grid * 2 * 4096)));
-    CKH(alloc_desc(h, (unsigned)std::max<unsigned long long>(8192, 16ull * h->grid)));
-    CKC(cudaMalloc(&h->bcounts, 3 * WHEEL * sizeof(unsigned)));
+    CKH(alloc_ring(h, std::max<unsigned long long>(opt.phantom_capacity > 0 ? cap : 2 * cap, (unsigned long long)h->grid * 2 * 4096)));
+    CKH(alloc_desc(h, 32));
+    CKC(cudaMalloc(&h->bcounts, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned)));
   } else {
     CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
     CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));
     CKC(cudaMalloc(&h->act[1], N * sizeof(unsigned)));
     CKH(alloc_pool(h, cap));
   }
+  set_l2_window(h);
   CKH(load_problem(h, p));
 #undef CKC
 #undef CKH

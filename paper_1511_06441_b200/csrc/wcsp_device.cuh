@@ -63,7 +63,7 @@ struct Acc {                       // per-cycle accumulators, triple-buffered by
   unsigned dmin;                   // min live residual after this cycle (0xFFFFFFFF = nothing live)
   unsigned long long bhit;         // max over B arrivals of (cand << 32 | ~X)
   unsigned long long live;         // sweep: live lanes at the top of the cycle (E); wheel: lanes started
-  unsigned long long arrivals, created, relabels, triggered;
+  unsigned long long arrivals, created, relabels, triggered, started, tested;
   long long pend_lanes, pend_phantoms;   // timing wheel: events in flight at the top of this cycle
 };
 
@@ -81,8 +81,9 @@ struct Ctl {
   unsigned abort, n_barr;          // barrier watchdog fired; B-arrival list length
   long long F1, F2, X, Y;
   long long via;
-  long long cycles, edge_updates, arrivals, triggered, created, relabels;
+  long long cycles, edge_updates, arrivals, triggered, created, relabels, started;
   long long peak_active, peak_phantoms, need_pool;
+  unsigned long long ts0, ts1, ts2;   // globaltimer at cycle start / after arrivals / after treat (block 0)
   // timing-wheel engine (wcsp_wheel.cuh)
   unsigned long long ev_head;      // logical allocation head of the event ring
   unsigned wheel_overflow, pad2_;  // 2: descriptor table full
@@ -90,7 +91,10 @@ struct Ctl {
   unsigned long long hist_head[WHEEL];   // ... and the ring head before its treat
 };
 
-struct TraceRec { long long t, delta, active_vertices, live_lanes, phantoms, triggered, arrivals, created, relabels; };
+struct TraceRec {
+  long long t, delta, active_vertices, live_lanes, phantoms, triggered, arrivals, created, relabels;
+  long long tested, ns_arrive, ns_treat;   // bitmap entries examined; phase times seen by block 0
+};
 
 struct Dev {
   unsigned N;
@@ -130,6 +134,58 @@ template <> struct Tr<3> { using LW = unsigned long long; };
 template <> struct Tr<4> { using LW = unsigned long long; };
 
 __host__ __device__ constexpr unsigned stamp_of(unsigned c) { return (c % STAMP_PERIOD) + 1u; }
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// L2 residency control (createpolicy + .L2::cache_hint): the vertex state
+// words are the hot, reused set (evict-last); events and weight records
+// stream through (evict-first).  WCSP_L2_HINTS=0 at build time disables it.
+#ifndef WCSP_L2_HINTS
+#define WCSP_L2_HINTS 1
+#endif
+__device__ __forceinline__ unsigned long long pol_first() {
+  unsigned long long p = 0;
+#if WCSP_L2_HINTS
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+__device__ __forceinline__ unsigned long long pol_last() {
+  unsigned long long p = 0;
+#if WCSP_L2_HINTS
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+__device__ __forceinline__ unsigned long long ld_hint(const unsigned long long* a, unsigned long long pol) {
+#if WCSP_L2_HINTS
+  unsigned long long v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol) : "memory");
+  return v;
+#else
+  return __ldcg(a);
+#endif
+}
+__device__ __forceinline__ void st_hint(unsigned long long* a, unsigned long long v, unsigned long long pol) {
+#if WCSP_L2_HINTS
+  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(pol) : "memory");
+#else
+  __stcs(a, v);
+#endif
+}
+__device__ __forceinline__ unsigned atom_max_hint(unsigned* a, unsigned v, unsigned long long pol) {
+#if WCSP_L2_HINTS
+  unsigned old;
+  asm volatile("atom.global.L2::cache_hint.max.u32 %0, [%1], %2, %3;" : "=r"(old) : "l"(a), "r"(v), "l"(pol) : "memory");
+  return old;
+#else
+  return atomicMax(a, v);
+#endif
+}
 
 __device__ __forceinline__ unsigned* tmp_ptr(unsigned long long* sw, unsigned v) {
   return reinterpret_cast<unsigned*>(sw + v) + 1;
@@ -177,6 +233,21 @@ template <int D> __device__ __forceinline__ WRec<typename Tr<D>::LW> load_wt(con
   }
   return r;
 }
+// streaming variant (evict-first): weight records of triggered vertices are
+// read once per cycle and must not push the vertex state words out of L2
+template <int D> __device__ __forceinline__ WRec<typename Tr<D>::LW> load_wt_cs(const Dev& s, unsigned v) {
+  using LW = typename Tr<D>::LW;
+  WRec<LW> r;
+  if constexpr (sizeof(LW) == 4) {
+    uint2 q = __ldcs(reinterpret_cast<const uint2*>(s.wt) + v);
+    r.f1 = q.x; r.f2 = q.y;
+  } else {
+    uint4 q = __ldcs(reinterpret_cast<const uint4*>(s.wt) + v);
+    r.f1 = ((unsigned long long)q.y << 32) | q.x;
+    r.f2 = ((unsigned long long)q.w << 32) | q.z;
+  }
+  return r;
+}
 template <int D> __device__ __forceinline__ typename Tr<D>::LW load_f2(const Dev& s, unsigned v) {
   if constexpr (sizeof(typename Tr<D>::LW) == 4) {
     return __ldg(reinterpret_cast<const unsigned*>(s.wt) + 2 * (size_t)v + 1);
@@ -201,7 +272,7 @@ struct Smem {
   unsigned base_a, base_b, flag;
   View view;
   unsigned long long bhit;
-  unsigned long long red[WARPS][5];
+  unsigned long long red[WARPS][7];
   unsigned redmin[WARPS];
 };
 
@@ -253,7 +324,8 @@ __device__ __forceinline__ void qflush(Smem& sm, unsigned* ga, unsigned* outa, u
 // block reductions -> one global atomic per counter per block
 __device__ __forceinline__ void block_reduce_commit(Smem& sm, unsigned dmin, unsigned long long a0,
                                                     unsigned long long a1, unsigned long long a2,
-                                                    unsigned long long a3, unsigned long long a4, Acc* acc) {
+                                                    unsigned long long a3, unsigned long long a4, Acc* acc,
+                                                    unsigned long long a5 = 0, unsigned long long a6 = 0) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     dmin = min(dmin, __shfl_xor_sync(0xFFFFFFFFu, dmin, o));
@@ -262,20 +334,26 @@ __device__ __forceinline__ void block_reduce_commit(Smem& sm, unsigned dmin, uns
     a2 += __shfl_xor_sync(0xFFFFFFFFu, a2, o);
     a3 += __shfl_xor_sync(0xFFFFFFFFu, a3, o);
     a4 += __shfl_xor_sync(0xFFFFFFFFu, a4, o);
+    a5 += __shfl_xor_sync(0xFFFFFFFFu, a5, o);
+    a6 += __shfl_xor_sync(0xFFFFFFFFu, a6, o);
   }
   const unsigned w = threadIdx.x >> 5;
   __syncthreads();
   if ((threadIdx.x & 31) == 0) {
     sm.redmin[w] = dmin;
     sm.red[w][0] = a0; sm.red[w][1] = a1; sm.red[w][2] = a2; sm.red[w][3] = a3; sm.red[w][4] = a4;
+    sm.red[w][5] = a5;
+    sm.red[w][6] = a6;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned m = 0xFFFFFFFFu;
-    unsigned long long s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+    unsigned long long s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0;
     for (int i = 0; i < WARPS; ++i) {
       m = min(m, sm.redmin[i]);
       s0 += sm.red[i][0]; s1 += sm.red[i][1]; s2 += sm.red[i][2]; s3 += sm.red[i][3]; s4 += sm.red[i][4];
+      s5 += sm.red[i][5];
+      s6 += sm.red[i][6];
     }
     if (m != 0xFFFFFFFFu) atomicMin(&acc->dmin, m);
     if (s0) atomicAdd(&acc->live, s0);
@@ -283,19 +361,10 @@ __device__ __forceinline__ void block_reduce_commit(Smem& sm, unsigned dmin, uns
     if (s2) atomicAdd(&acc->created, s2);
     if (s3) atomicAdd(&acc->relabels, s3);
     if (s4) atomicAdd(&acc->triggered, s4);
+    if (s5) atomicAdd(&acc->started, s5);
+    if (s6) atomicAdd(&acc->tested, s6);
   }
   __syncthreads();
-}
-
-// Set bit D of the triggered bitmap for every predicated lane; lanes hitting
-// the same word combine first (one atomicOr per word per warp).
-__device__ __forceinline__ void bit_set(unsigned* bits, bool pred, unsigned D) {
-  const unsigned m = __ballot_sync(0xFFFFFFFFu, pred);
-  if (m == 0 || !pred) return;
-  const unsigned word = D >> 5;
-  const unsigned peers = __match_any_sync(m, word);
-  const unsigned acc = __reduce_or_sync(peers, 1u << (D & 31u));
-  if ((threadIdx.x & 31u) == (unsigned)(__ffs(peers) - 1)) atomicOr(bits + word, acc);
 }
 
 // Water of quality `cand` reaches D from `src` (quality <= 0
@@ -304,25 +373,26 @@ __device__ __forceinline__ void bit_set(unsigned* bits, bool pred, unsigned D) {
 // first time this cycle.  The comparison with L(D) ("L(S) - f2(e) > L(D)",
 // :32) is made once per triggered vertex in treat: max over all arrivals
 // beats L(D) iff max over the accepted ones does, and then they are equal
-// (reading R-new-1).  Must be called by all 32 lanes of the warp.
-__device__ __forceinline__ void arrive(const Dev& s, const View& v, Acc* acc, bool go, unsigned D, int cand,
-                                       unsigned src, unsigned via) {
-  go = go && cand > 0;
-  bool first = false;
-  if (go) {
-    const unsigned old = atomicMax(tmp_ptr(s.sw, D), (v.stamp << 16) | (unsigned)cand);
-    const unsigned os = old >> 16;
-    if (os == 0xFFFFu) {
-      if (old == TMP_B) {          // termination 1°: a vertex of B is reached
-        atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - D));
-        const unsigned k = atomicAdd(&s.ctl->n_barr, 1u);
-        if (k < s.barr_cap) s.barr[k] = BArr{D, (unsigned)cand, src, via};
-      }
-    } else {
-      first = os != v.stamp;
+// (reading R-new-1).  Split in two so a thread can put several atomics in
+// flight before it needs their results: arrive_atomic issues the atomicMax,
+// arrive_post acts on its return value (the bitmap OR is a fire-and-forget
+// reduction).
+__device__ __forceinline__ unsigned arrive_atomic(const Dev& s, const View& v, bool go, unsigned D, int cand) {
+  return go ? atom_max_hint(tmp_ptr(s.sw, D), (v.stamp << 16) | (unsigned)cand, pol_last()) : (v.stamp << 16);
+}
+
+__device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* acc, unsigned old, unsigned D,
+                                            int cand, unsigned src, unsigned via) {
+  const unsigned os = old >> 16;
+  if (os == 0xFFFFu) {
+    if (old == TMP_B) {            // termination 1°: a vertex of B is reached
+      atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - D));
+      const unsigned k = atomicAdd(&s.ctl->n_barr, 1u);
+      if (k < s.barr_cap) s.barr[k] = BArr{D, (unsigned)cand, src, via};
     }
+  } else if (os != v.stamp) {      // first arrival of the cycle: D is triggered (dedupe)
+    atomicOr(s.tbits + (D >> 5), 1u << (D & 31u));
   }
-  bit_set(s.tbits, first, D);
 }
 
 // ---------------------------------------------------------------------------
@@ -382,12 +452,19 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
       }
 #pragma unroll
       for (int it = 0; it < SWEEP_ITEMS; ++it) {
+        if (!fired[it]) continue;
+        unsigned old[2 * D];
 #pragma unroll
         for (int j = 0; j < 2 * D; ++j) {
           const bool fj = (fired[it] >> (8 * j + 7)) & 1;
           arr += fj;
           const int cand = (int)lbl[it] - (int)((f2w[it] >> (8 * j)) & 0xFF);
-          arrive(s, v, acc, fj, vx[it] + s.off[j], cand, vx[it], 0u);
+          old[j] = arrive_atomic(s, v, fj && cand > 0, vx[it] + s.off[j], cand);
+        }
+#pragma unroll
+        for (int j = 0; j < 2 * D; ++j) {
+          const int cand = (int)lbl[it] - (int)((f2w[it] >> (8 * j)) & 0xFF);
+          arrive_post(s, v, acc, old[j], vx[it] + s.off[j], cand, vx[it], 0u);
         }
       }
     } else {
@@ -398,6 +475,7 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
         const unsigned i = pc * chunk + it * THREADS + threadIdx.x;
         p[it] = ((unsigned)it < items && i < v.n_pool) ? __ldcs(pool_in + i) : 0ull;
       }
+      unsigned old[SWEEP_ITEMS];
 #pragma unroll
       for (int it = 0; it < SWEEP_ITEMS; ++it) {
         const unsigned r = (unsigned)(p[it] >> PH_RES) & 0xFFu;   // 0 only for padding
@@ -409,8 +487,13 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
                                   &acc->n_pool, pool_out, s.pool_cap);
         const unsigned src = (unsigned)p[it] & 0x3FFFFFFFu;
         const unsigned lane = (unsigned)(p[it] >> PH_LANE) & 7u;
-        const int cand = (int)((p[it] >> PH_CAND) & 0xFFFFu);
-        arrive(s, v, acc, fire, src + s.off[lane], cand, src, 1u);
+        old[it] = arrive_atomic(s, v, fire, src + s.off[lane], (int)((p[it] >> PH_CAND) & 0xFFFFu));
+      }
+#pragma unroll
+      for (int it = 0; it < SWEEP_ITEMS; ++it) {
+        const unsigned src = (unsigned)p[it] & 0x3FFFFFFFu;
+        const unsigned lane = (unsigned)(p[it] >> PH_LANE) & 7u;
+        arrive_post(s, v, acc, old[it], src + s.off[lane], (int)((p[it] >> PH_CAND) & 0xFFFFu), src, 1u);
       }
     }
     qflush(sm, &acc->n_act, act_out, &acc->n_pool, pool_out, s.pool_cap);
@@ -457,7 +540,7 @@ template <int D, bool WHEEL_ENGINE>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
                                           unsigned& dmin, unsigned long long& created,
                                           unsigned long long& relabels, unsigned long long& triggered,
-                                          unsigned long long& lanes_started);
+                                          unsigned long long& lanes_started, unsigned long long& tested);
 
 __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
   return ((texp16 - (unsigned)t) & 0xFFFFu) - 1u < 255u;   // texp in (t, t + 255]
@@ -470,11 +553,12 @@ template <int D, bool WHEEL_ENGINE>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
                                           unsigned& dmin, unsigned long long& created,
                                           unsigned long long& relabels, unsigned long long& triggered,
-                                          unsigned long long& lanes_started) {
+                                          unsigned long long& lanes_started, unsigned long long& tested) {
   using LW = typename Tr<D>::LW;
   const bool valid = q != 0xFFFFFFFFu;
-  const unsigned long long swq = valid ? __ldcg(s.sw + q) : 0ull;
-  const WRec<LW> wr = valid ? load_wt<D>(s, q) : WRec<LW>{0, 0};
+  tested += valid;
+  const unsigned long long swq = valid ? ld_hint(s.sw + q, pol_last()) : 0ull;
+  const WRec<LW> wr = valid ? load_wt_cs<D>(s, q) : WRec<LW>{0, 0};
   LW w = 0;
   if constexpr (!WHEEL_ENGINE) w = valid ? __ldcg(reinterpret_cast<LW*>(s.res) + q) : (LW)0;
   const int lq = (int)(swq & 0xFFFFu);
@@ -490,7 +574,9 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
     const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
     const bool test = trig && f1j != 0 && lstar - (int)f2j > 0;
-    swr[j] = test ? __ldcg(s.sw + (q + s.off[j])) : 0xFFFFull;    // untested lanes read as "removed"
+    // L1-cached read: this phase never writes the temp half, the label half only moves to
+    // max(L, temp) (benign), and the grid barrier before the phase invalidated L1
+    swr[j] = test ? s.sw[q + s.off[j]] : 0xFFFFull;   // untested lanes read as "removed"
   }
   LW neww = 0;
   unsigned fmax = 0;
@@ -543,26 +629,28 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   Acc* acc = &s.ctl->acc[v.c % 3];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const unsigned nwin = (s.nwords + WIN_WORDS - 1) / WIN_WORDS;
-  const unsigned per_round = gridDim.x * WARPS;
+  // every block owns one contiguous slab of windows: its phantoms / events come from a
+  // compact region of the grid, so a run's destinations share sectors and L2 lines
+  const unsigned rounds = (nwin + gridDim.x * WARPS - 1) / (gridDim.x * WARPS);
+  const unsigned win0 = blockIdx.x * rounds * WARPS;
   unsigned dmin = 0xFFFFFFFFu;
-  unsigned long long created = 0, relabels = 0, triggered = 0, lanes_started = 0;
+  unsigned long long created = 0, relabels = 0, triggered = 0, lanes_started = 0, tested = 0;
   if constexpr (WHEEL_ENGINE) {
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.rcap[d] = 0; sm.rfill[d] = 0; }
     __syncthreads();
   }
-  for (unsigned r0 = 0; r0 < nwin; r0 += per_round) {
-    const unsigned win = r0 + blockIdx.x * WARPS + warp;
+  for (unsigned r = 0; r < rounds; ++r) {
+    const unsigned win = win0 + r * WARPS + warp;
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
       const unsigned q = b + lane < total ? sm.wl[warp][b + lane] : 0xFFFFFFFFu;
-      treat_one<D, WHEEL_ENGINE>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started);
+      treat_one<D, WHEEL_ENGINE>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
     }
     if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, false);
     else qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
   }
   if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, true);
-  // wheel: lanes started ride in the 'live' slot (the sweep counts live lanes there in its sweep)
-  block_reduce_commit(sm, dmin, WHEEL_ENGINE ? lanes_started : 0ull, 0, created, relabels, triggered, acc);
+  block_reduce_commit(sm, dmin, 0, 0, created, relabels, triggered, acc, lanes_started, tested);
 }
 
 // ---------------------------------------------------------------------------
@@ -571,7 +659,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
 __device__ __forceinline__ void reset_acc(Acc* a) {
   a->n_act = 0; a->n_pool = 0; a->n_trig = 0; a->dmin = 0xFFFFFFFFu;
   a->bhit = 0; a->live = 0; a->arrivals = 0; a->created = 0; a->relabels = 0; a->triggered = 0;
-  a->pend_lanes = 0; a->pend_phantoms = 0;
+  a->started = 0; a->tested = 0; a->pend_lanes = 0; a->pend_phantoms = 0;
 }
 
 __device__ __forceinline__ void resolve_hit(const Dev& s, unsigned long long bhit, long long t) {
@@ -602,12 +690,15 @@ __device__ void decide(const Dev& s, View& v, bool writer) {
     const unsigned long long live = __ldcg(&a->live), arrivals = __ldcg(&a->arrivals);
     const unsigned long long created = __ldcg(&a->created), relabels = __ldcg(&a->relabels);
     const unsigned long long triggered = __ldcg(&a->triggered);
+    C->started += (long long)__ldcg(&a->started);
     if (v.c > 0) {
       C->cycles += 1;
       C->edge_updates += (long long)(live + v.n_pool);
       if ((long long)v.c - 1 < s.trace_cap) {
+        const unsigned long long t2 = globaltimer_ns();
         TraceRec r{v.t, (long long)v.delta, (long long)v.n_act, (long long)live, (long long)v.n_pool,
-                   (long long)triggered, (long long)arrivals, (long long)created, (long long)relabels};
+                   (long long)triggered, (long long)arrivals, (long long)created, (long long)relabels,
+                   (long long)__ldcg(&a->tested), (long long)(C->ts1 - C->ts0), (long long)(t2 - C->ts1)};
         s.trace[v.c - 1] = r;
       }
     }
@@ -647,12 +738,6 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
-}
-
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
 }
 
 // Returns false if the barrier was abandoned (watchdog: a block missing for
@@ -720,11 +805,15 @@ __global__ void __launch_bounds__(THREADS, 4) k_persistent(Dev s) {
   unsigned long long target = 0;
   while (v.status == ST_RUNNING) {
     if (v.c > 0) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
+        s.ctl->ts0 = globaltimer_ns();
+      }
       phase_sweep<D>(s, v, sm);
       target += G;
       if (!grid_sync(s.ctl, target, sm)) return;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
     if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
     __syncthreads();
     const unsigned long long bhit = sm.bhit;
@@ -757,7 +846,10 @@ __global__ void __launch_bounds__(THREADS, 4) k_sweep(Dev s) {
   View v;
   load_view(s, sm, v);
   if (v.status != ST_RUNNING || v.c == 0) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
+    s.ctl->ts0 = globaltimer_ns();
+  }
   phase_sweep<D>(s, v, sm);
 }
 
@@ -768,6 +860,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_treat(Dev s) {
   View v;
   load_view(s, sm, v);
   if (v.status != ST_RUNNING) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
   if (__ldcg(&s.ctl->acc[v.c % 3].bhit)) return;
   phase_treat<D, false>(s, v, sm);
 }

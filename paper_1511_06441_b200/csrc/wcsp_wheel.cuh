@@ -29,10 +29,16 @@ namespace wcspk {
 constexpr int EV_LANE_BIT = 49;
 constexpr int EV_DELAY_SHIFT = 56;
 constexpr unsigned MAINT_PERIOD_T = 1u << 15;
+constexpr int FIRE_ITEMS = 8;             // events per lane per fire chunk (atomics in flight)
 
+// Runs are filed per (bucket, block): the block that treats a slab of the grid
+// also fires the events its slab created, so the atomics of a fire phase
+// walk compact regions of the state array (L2-resident) instead of the
+// whole front at once.
 __device__ __forceinline__ void file_run(const Dev& s, unsigned b, unsigned long long pos, unsigned cnt) {
-  const unsigned k = atomicAdd(s.bndesc + b, 1u);
-  if (k < s.dcap) s.bdesc[(size_t)b * s.dcap + k] = (pos << 24) | cnt;
+  const size_t slot = (size_t)b * s.nblocks + blockIdx.x;
+  const unsigned k = atomicAdd(s.bndesc + slot, 1u);
+  if (k < s.dcap) s.bdesc[slot * s.dcap + k] = (pos << 24) | cnt;
   else atomicOr(&s.ctl->wheel_overflow, 2u);
 }
 
@@ -96,7 +102,7 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
     for (unsigned i = threadIdx.x; i < n; i += THREADS) {
       const unsigned long long e = sm.qp[i];
       const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
-      s.ev[(sm.hbase[d] + sm.rank[i]) & s.ev_mask] = e & ((1ull << EV_DELAY_SHIFT) - 1);
+      st_hint(s.ev + ((sm.hbase[d] + sm.rank[i]) & s.ev_mask), e & ((1ull << EV_DELAY_SHIFT) - 1), pol_first());
     }
     __syncthreads();
     if (threadIdx.x == 0) sm.np = 0;
@@ -114,41 +120,86 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
 // Start-of-cycle bookkeeping (block 0, thread 0, before the fire phase).
 __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
   reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
+  s.ctl->ts0 = globaltimer_ns();
   const unsigned prev = (unsigned)((v.t - v.delta) & (WHEEL - 1));   // the bucket fired last cycle
-  s.bndesc[prev] = 0; s.bnev[prev] = 0; s.bnlane[prev] = 0;
+  s.bnev[prev] = 0; s.bnlane[prev] = 0;
   s.ctl->hist_t[v.c & (WHEEL - 1)] = v.t;
   s.ctl->hist_head[v.c & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
 }
 
-// fire: the events of bucket t reach their destinations (Steps 1-3), one warp per run.
+// fire: the events of bucket t reach their destinations (Steps 1-3).  Block k
+// fires the runs its own slab filed; the runs are cut into chunks of
+// FIRE_ITEMS * 32 events that the block's warps take in turn (a prefix sum of
+// chunk counts over the block's runs lives in shared memory).
 template <int D>
 __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   Acc* acc = &s.ctl->acc[v.c % 3];
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
-  const unsigned nd = min(__ldcg(s.bndesc + b), s.dcap);
-  const unsigned lane = threadIdx.x & 31u;
-  const unsigned gw = blockIdx.x * WARPS + (threadIdx.x >> 5), nw = gridDim.x * WARPS;
+  if (threadIdx.x == 0) s.bndesc[(size_t)((v.t - v.delta) & (WHEEL - 1)) * s.nblocks + blockIdx.x] = 0;
+  const size_t slot = (size_t)b * s.nblocks + blockIdx.x;
+  const unsigned nd = min(__ldcg(s.bndesc + slot), s.dcap);
+  const unsigned long long* dl = s.bdesc + slot * s.dcap;
+  constexpr unsigned CH = FIRE_ITEMS * 32;
+  constexpr unsigned MAXD = 512;
+  unsigned long long* dpos = reinterpret_cast<unsigned long long*>(&sm.wl[0][0]);   // [MAXD]
+  unsigned* dchunk = &sm.wl[0][0] + 2 * MAXD;                                         // [MAXD + 1] prefix
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   unsigned long long arr = 0;
-  for (unsigned di = gw; di < nd; di += nw) {
-    const unsigned long long dsc = __ldcg(s.bdesc + (size_t)b * s.dcap + di);
-    const unsigned long long pos = dsc >> 24;
-    const unsigned cnt = (unsigned)(dsc & 0xFFFFFFu);
-    for (unsigned base = 0; base < cnt; base += 4 * 32) {
-      unsigned long long e[4];
+  for (unsigned d0 = 0; d0 < nd; d0 += MAXD) {
+    const unsigned n = min(MAXD, nd - d0);
+    __syncthreads();
+    if (warp == 0) {                 // prefix sum of chunk counts (warp 0, MAXD / 32 passes)
+      unsigned carry = 0;
+      for (unsigned i0 = 0; i0 < n; i0 += 32) {
+        const unsigned i = i0 + lane;
+        unsigned long long dsc = 0;
+        unsigned ch = 0;
+        if (i < n) {
+          dsc = __ldcg(dl + d0 + i);
+          ch = ((unsigned)(dsc & 0xFFFFFFu) + CH - 1) / CH;
+          dpos[i] = dsc;
+        }
+        unsigned x = ch;
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const unsigned i = base + it * 32 + lane;
-        e[it] = i < cnt ? __ldcs(s.ev + ((pos + i) & s.ev_mask)) : ~0ull;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+          if ((int)lane >= o) x += y;
+        }
+        if (i < n) dchunk[i] = carry + x - ch;
+        carry += __shfl_sync(0xFFFFFFFFu, x, 31);
       }
+      if (lane == 0) dchunk[n] = carry;
+    }
+    __syncthreads();
+    const unsigned nchunks = dchunk[n];
+    unsigned di = 0;
+    for (unsigned c = warp; c < nchunks; c += WARPS) {
+      while (dchunk[di + 1] <= c) ++di;          // chunks are visited in increasing order
+      const unsigned long long dsc = dpos[di];
+      const unsigned long long pos = dsc >> 24;
+      const unsigned cnt = (unsigned)(dsc & 0xFFFFFFu);
+      const unsigned base = (c - dchunk[di]) * CH;
+      unsigned long long e[FIRE_ITEMS];
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {
+      for (int it = 0; it < FIRE_ITEMS; ++it) {
+        const unsigned i = base + it * 32 + lane;
+        e[it] = i < cnt ? ld_hint(s.ev + ((pos + i) & s.ev_mask), pol_first()) : ~0ull;
+      }
+      unsigned old[FIRE_ITEMS];
+#pragma unroll
+      for (int it = 0; it < FIRE_ITEMS; ++it) {   // put every atomic in flight before using a result
         const bool valid = e[it] != ~0ull;
         arr += valid;
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
-        const int cand = (int)((e[it] >> PH_CAND) & 0xFFFFu);
+        old[it] = arrive_atomic(s, v, valid, src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));
+      }
+#pragma unroll
+      for (int it = 0; it < FIRE_ITEMS; ++it) {
+        const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
+        const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
         const unsigned via = ((e[it] >> EV_LANE_BIT) & 1) ? 0u : 1u;
-        arrive(s, v, acc, valid, src + s.off[ln], cand, src, via);
+        arrive_post(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu), src, via);
       }
     }
   }
@@ -167,7 +218,7 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
   const long long pp = __ldcg((const long long*)&a->pend_phantoms);   // P at the top of this cycle
   const long long fired = v.c > 0 ? (long long)__ldcg(s.bnev + b) : 0;
   const long long fired_l = v.c > 0 ? (long long)__ldcg(s.bnlane + b) : 0;
-  const long long new_l = (long long)__ldcg(&a->live);                // lanes started this cycle
+  const long long new_l = (long long)__ldcg(&a->started);             // lanes started this cycle
   const long long new_p = (long long)__ldcg(&a->created);             // phantoms created this cycle
   const long long npl = pl - fired_l + new_l, npp = pp - (fired - fired_l) + new_p;
   if (writer) {
@@ -177,12 +228,15 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
       C->cycles += 1;
       C->edge_updates += pl + pp;
       if ((long long)v.c - 1 < s.trace_cap) {
-        TraceRec r{v.t, (long long)v.delta, -1, pl, pp, (long long)triggered, (long long)arrivals, new_p,
-                   (long long)relabels};
+        const unsigned long long t2 = globaltimer_ns();
+        TraceRec r{v.t, (long long)v.delta, (long long)__ldcg(s.bndesc + (size_t)b * s.nblocks), pl, pp, (long long)triggered, (long long)arrivals, new_p,
+                   (long long)relabels, (long long)__ldcg(&a->tested), (long long)(C->ts1 - C->ts0),
+                   (long long)(t2 - C->ts1)};
         s.trace[v.c - 1] = r;
       }
     }
     C->arrivals += arrivals; C->triggered += triggered; C->created += new_p; C->relabels += relabels;
+    C->started += new_l;
   }
   if (bhit) {
     nv.status = 0;
@@ -267,6 +321,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_wheel_persistent(Dev s) {
       target += G;
       if (!grid_sync(s.ctl, target, sm)) return;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
     if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
     __syncthreads();
     const unsigned long long bhit = sm.bhit;
@@ -311,6 +366,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_wheel_treat(Dev s) {
   View v;
   load_view(s, sm, v);
   if (v.status != ST_RUNNING) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
   if (__ldcg(&s.ctl->acc[v.c % 3].bhit)) return;
   phase_treat<D, true>(s, v, sm);
 }

@@ -55,14 +55,14 @@ class _Result(ctypes.Structure):
                 ("x_lane", ctypes.c_int32), ("via_phantom", ctypes.c_int32),
                 ("cycles", ctypes.c_int64), ("edge_updates", ctypes.c_int64), ("arrivals", ctypes.c_int64),
                 ("triggered", ctypes.c_int64), ("phantoms_created", ctypes.c_int64),
-                ("relabels", ctypes.c_int64), ("peak_active", ctypes.c_int64),
+                ("relabels", ctypes.c_int64), ("lanes_started", ctypes.c_int64), ("peak_active", ctypes.c_int64),
                 ("peak_phantoms", ctypes.c_int64), ("phantom_capacity", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("device_ms", ctypes.c_double),
                 ("cycle_ms", ctypes.c_double)]
 
 
 TRACE_FIELDS = ["t", "delta", "active_vertices", "live_lanes", "phantoms", "triggered", "arrivals",
-                "created", "relabels"]
+                "created", "relabels", "tested", "ns_arrive", "ns_treat"]
 
 
 class _TraceRec(ctypes.Structure):
@@ -126,6 +126,7 @@ class Result:
     triggered: int = 0
     phantoms_created: int = 0
     relabels: int = 0
+    lanes_started: int = 0
     peak_active: int = 0
     peak_phantoms: int = 0
     phantom_capacity: int = 0
@@ -252,7 +253,7 @@ class Solver:
         st = self._lib.wcsp_trace(self._h, buf, cap, ctypes.byref(n))
         if st != REACHED:
             raise WcspError(st, last_error())
-        arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_int64)), shape=(cap, 9))[: n.value]
+        arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ctypes.c_int64)), shape=(cap, len(TRACE_FIELDS)))[: n.value]
         return {f: arr[:, i].copy() for i, f in enumerate(TRACE_FIELDS)}
 
     def close(self):

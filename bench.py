@@ -37,6 +37,8 @@ WORKLOADS = {
     "C2": {"shape": (1024, 1024), "desc": "configs[1]: 2D 1024^2, f1,f2 ~ U{1..10}, A = left face, B = right face, "
                                           "M = M_bind"},
     "C3s": {"shape": (128, 128, 128), "desc": "128^3 cube (reduced C3 for quick runs), M = M_bind"},
+    "C4": {"shape": None, "desc": "configs[3]: Theorem-2 fractal omega_k, k = 10 (t = 1024), V = [-t,t]x[0,t+1], "
+                                  "A = x-axis, B = (0,t), f1 in {1,2}, f2 = 1, M = infinity"},
 }
 MBIND = os.path.join(ROOT, "paper_1511_06441_b200", "data", "mbind.json")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "roofline_traffic.json")
@@ -48,6 +50,9 @@ def dist_env():
 
 def workload_instance(name: str, seed: int):
     from paper_1511_06441_b200 import instances as I
+    if name == "C4":
+        inst = I.fractal_instance(10)
+        return inst, {"seed": 0, "F1_lex": 1024, "M_bind": I.M_INF}
     table = json.load(open(MBIND))
     key = f"{name}/{seed}"
     if key not in table:

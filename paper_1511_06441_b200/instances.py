@@ -259,6 +259,100 @@ def speedway_instance(n: int, M: int = M_INF, B=None) -> Instance:
     return Instance(shape, f1, f2, mA, mB, M, None, f"speedway{n}")
 
 
+def _staircase(p, q):
+    """Unit lattice staircase from p to q (|dx| = |dy|), x-step first
+    (SPEC.md:406 rasterisation; SURVEY reading R26).  Returns the edges as
+    ((x, y), (x', y')) pairs."""
+    (x, y), (x1, y1) = p, q
+    n = abs(x1 - x)
+    assert n == abs(y1 - y), (p, q)
+    sx, sy = (1 if x1 > x else -1), (1 if y1 > y else -1)
+    out = []
+    for _ in range(n):
+        out.append(((x, y), (x + sx, y)))
+        x += sx
+        out.append(((x, y), (x, y + sy)))
+        y += sy
+    return out
+
+
+def _vertical(p, q):
+    (x, y), (x1, y1) = p, q
+    assert x == x1
+    lo, hi = min(y, y1), max(y, y1)
+    return [((x, yy), (x, yy + 1)) for yy in range(lo, hi)]
+
+
+def fractal_fast_edges(k: int):
+    """Fast (f1 = 1) edges of the Theorem-2 environment omega_k
+    on the left half-plane: the y-axis and segment LO (omega_1),
+    then k - 1 refinements; refining a triangle (a, b, c) similar to (L, O, T)
+    adds the vertical mid(a,b) -> mid(a,c) and the diagonal mid(c,b) -> mid(a,c)
+    (the segments L0X and T0X of PAPER.md:303) and recurses into
+    (a, mid(a,b), mid(a,c)) and (mid(a,c), mid(c,b), c) (I_2 of PAPER.md:303).
+    t = 2^k; L = (-t/2, 0), O = (0, t/2), T = (0, t) (PAPER.md:293)."""
+    t = 1 << k
+    L, O, T = (-t // 2, 0), (0, t // 2), (0, t)
+    edges = set(_vertical((0, 0), (0, t)))            # the y-axis
+    edges.update(_staircase(L, O))                    # segment LO
+    mid = lambda p, q: ((p[0] + q[0]) // 2, (p[1] + q[1]) // 2)
+    tris = [(L, O, T)]
+    for _ in range(k - 1):
+        nxt = []
+        for a, b, c in tris:
+            mab, mac, mcb = mid(a, b), mid(a, c), mid(c, b)
+            edges.update(_vertical(mab, mac))
+            edges.update(_staircase(mcb, mac))
+            nxt += [(a, mab, mac), (mac, mcb, c)]
+        tris = nxt
+    return edges
+
+
+def fractal_instance(k: int, M: int = M_INF, B=None) -> Instance:
+    """configs[3]: the paper's fractal active-set construction (Theorem 2,
+    PAPER.md:290-349) on V = [-t, t] x [0, t + 1] (PAPER.md:253 with n = t + 1,
+    SURVEY §8(d) C4), t = 2^k, water on the whole x-axis, f1 = 1 on omega_k's
+    fast edges (mirrored across the y-axis) and 2 elsewhere
+    (PAPER.md:255), f2 = 1; B = {(0, t)} by default."""
+    t = 1 << k
+    shape = (2 * t + 1, t + 2)
+    N = shape[0] * shape[1]
+    f1 = np.full((2, N), 2, dtype=np.uint8)
+    f2 = np.ones((2, N), dtype=np.uint8)
+    v = np.arange(N)
+    xa, ya = v % shape[0], v // shape[0]
+    for kk, last in ((0, xa == shape[0] - 1), (1, ya == shape[1] - 1)):
+        f1[kk, last] = 0
+        f2[kk, last] = 0
+    for (p, q) in fractal_fast_edges(k):
+        for sgn in (1, -1):                            # mirror across x = 0
+            (x0, y0), (x1, y1) = (sgn * p[0], p[1]), (sgn * q[0], q[1])
+            if (x1, y1) < (x0, y0):
+                (x0, y0), (x1, y1) = (x1, y1), (x0, y0)
+            kk = 0 if y0 == y1 else 1
+            f1[kk, (x0 + t) + shape[0] * y0] = 1
+    mA = (ya == 0).astype(np.uint8)
+    mB = np.zeros(N, np.uint8)
+    for (x, y) in (B or [(0, t)]):
+        mB[(x + t) + shape[0] * y] = 1
+    return Instance(shape, f1, f2, mA, mB, M, None, f"fractal{k}")
+
+
+def speedway_lemma_set(T: int):
+    """The §5 Lemma's active set at time T with the
+    correction of SURVEY E1 / reading R15 (exact for every T >= 3 under eager
+    retirement): Lemma ∪ {(±k, T - 2k - 1) : 1 <= k <= floor((T - 3) / 4)}.
+    Returned as (finite core, height of the flat part, |z| bound of the core):
+    the flat part is {(z, floor(T/2)) : |z| > floor((T+1)/4)}."""
+    m = (T + 1) // 4
+    core = {(0, T), (0, T - 1)}
+    for k in range(1, m + 1):
+        core |= {(-k, T - 2 * k), (k, T - 2 * k)}
+    for k in range(1, (T - 3) // 4 + 1):
+        core |= {(-k, T - 2 * k - 1), (k, T - 2 * k - 1)}
+    return core, T // 2, m
+
+
 def random_small(rng: np.random.Generator, shapes=None, lo_hi=None, M_range=(3, 60),
                  max_sources=3, max_targets=3, hole_prob=0.0) -> Instance:
     """Random small instance for property suites: random shape from `shapes`,

@@ -225,3 +225,44 @@ def test_C3_full_size_M_endpoints_and_properties():
         assert rb.status == wcsp.REACHED and rb.F2 < Mb and hi.F1 <= rb.F1 <= lo.F1
         s.set_targets(M=Mb + 25)
         assert s.solve().F1 <= rb.F1
+
+
+def test_speedway_active_vertex_sequence():
+    """§5 Lemma environment, M = infinity, unit time: the sweep
+    engine's active-vertex sequence (PAPER.md:143; trace 'active_vertices' at
+    the top of cycle T + 1) equals the method's active set at time T computed
+    from first-passage times, which tests/test_oracle.py ties to the corrected
+    Lemma (reading R15)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_oracle import first_passage, speedway_sets
+    n = 48
+    s = I.speedway_instance(n)
+    tau = first_passage(s)
+    with wcsp.Solver(s, time_mode="unit", trace_cap=256) as sv:
+        r = sv.solve()
+        tr = sv.trace()
+    assert r.F1 == n
+    checked = 0
+    for i, t in enumerate(tr["t"]):
+        T = int(t) - 1
+        if 3 <= T <= 44:
+            _, lazy = speedway_sets(n, T, tau, s)
+            assert tr["active_vertices"][i] == len(lazy), T
+            checked += 1
+    assert checked == 42
+
+
+@pytest.mark.parametrize("engine", ["persistent", "wheel"])
+def test_fractal_C4(engine):
+    """configs[3] (Theorem-2 fractal): F1 = t = 2^k (SURVEY
+    P7); with M = t + 1 the unique feasible path is the y-axis."""
+    for k in range(3, 10):
+        f = I.fractal_instance(k)
+        t = 1 << k
+        r = wcsp.solve(f, engine=engine)
+        assert r.key() == oracle.solve_lex(f, 2).key() and r.F1 == t
+        assert r.phantoms_created == 0
+        want = (wcsp.REACHED, t, t, f.index((t, t)), f.index((t, t - 1)))
+        r2 = wcsp.solve(f.with_M(t + 1), engine=engine)
+        assert r2.key() == want

@@ -226,3 +226,105 @@ def test_generator_is_deterministic_and_uniform():
     counts = np.bincount(vals, minlength=11)[1:]
     assert counts.min() > 0.8 * counts.mean()
     assert np.corrcoef(a1[a1 > 0], a2[a1 > 0])[0, 1] < 0.05   # f1 independent of f2 (R19)
+
+
+# ---------------------------------------------------------------------------
+# §5: speedway Lemma (corrected, SURVEY E1 / reading R15) and the Theorem-2
+# fractal's closed form
+# ---------------------------------------------------------------------------
+
+def first_passage(inst):
+    """tau(v): plain Dijkstra on f1 from A (textbook, independent of oracle/)."""
+    import heapq
+    st = I.strides(inst.shape)
+    dist = np.full(inst.N, 1 << 60, dtype=np.int64)
+    pq = []
+    for v in np.flatnonzero(inst.maskA):
+        dist[v] = 0
+        pq.append((0, int(v)))
+    heapq.heapify(pq)
+    while pq:
+        d, v = heapq.heappop(pq)
+        if d > dist[v]:
+            continue
+        for u, a, _ in py_neighbours(inst, v):
+            if d + a < dist[u]:
+                dist[u] = d + a
+                heapq.heappush(pq, (d + a, u))
+    return dist
+
+
+def speedway_sets(n, T, tau, inst):
+    """(eager, lazy) active sets at time T from first-passage times: eager =
+    reached and some neighbour not yet reached (the Lemma's notion); lazy =
+    some edge started at tau(v) toward a later-reached neighbour is still in
+    flight after T (the method's active-vertex sequence)."""
+    eager, lazy = set(), set()
+    for v in range(inst.N):
+        if tau[v] > T:
+            continue
+        x, y = inst.coords(v)
+        nb = py_neighbours(inst, v)
+        if any(tau[u] > T for u, _, _ in nb):
+            eager.add((x - n, y))
+        if any(tau[u] > tau[v] and tau[v] + a > T for u, a, _ in nb):
+            lazy.add((x - n, y))
+    return eager, lazy
+
+
+def lemma_printed(T, n):
+    """The Lemma exactly as printed."""
+    m = (T + 1) // 4
+    s = {(0, T), (0, T - 1)}
+    for k in range(1, m + 1):
+        s |= {(-k, T - 2 * k), (k, T - 2 * k)}
+    return s | {(z, T // 2) for z in range(-n, n + 1) if abs(z) > m}
+
+
+def test_speedway_lemma_corrected():
+    """The Lemma's active set, checked against first-passage times on the
+    lattice (the proof's own argument): the printed form is
+    exact for T <= 6 only; the corrected form (R15) is exact for every T; the
+    method's (lazy) active sequence adds (±k, 2k) when T = 4k + 1 and
+    (±k, 2k + 1) when T = 4k + 2 (an edge still in flight toward a neighbour
+    that was reached another way)."""
+    n = 40
+    s = I.speedway_instance(n)
+    tau = first_passage(s)
+    printed_fails = []
+    for T in range(3, 41):
+        eager, lazy = speedway_sets(n, T, tau, s)
+        core, h, m = I.speedway_lemma_set(T)
+        corrected = set(core) | {(z, h) for z in range(-n, n + 1) if abs(z) > m}
+        assert eager == corrected, T
+        if lemma_printed(T, n) != eager:
+            printed_fails.append(T)
+        extra = set()
+        for k in range(1, T):
+            if T == 4 * k + 1:
+                extra |= {(-k, 2 * k), (k, 2 * k)}
+            if T == 4 * k + 2:
+                extra |= {(-k, 2 * k + 1), (k, 2 * k + 1)}
+        assert lazy == eager | extra, T
+    assert printed_fails and min(printed_fails) == 7
+
+
+def test_fractal_closed_form_P7():
+    """Theorem-2 environment: F1 to (0, t) is t = 2^k (the
+    fast y-axis; any path needs t vertical steps); with f2 = 1 and M = t + 1 the
+    only feasible path is the y-axis itself: F2 = t, X = (0, t), Y = (0, t-1)."""
+    for k in range(2, 8):
+        f = I.fractal_instance(k)
+        t = 1 << k
+        assert oracle.solve_lex(f, 2).F1 == t
+        assert oracle.solve_pruned(f).F1 == t
+        want = (oracle.REACHED, t, t, f.index((t, t)), f.index((t, t - 1)))
+        assert oracle.solve_pruned(f.with_M(t + 1)).key() == want
+        assert oracle.solve_lex(f, 1).key() == want          # M = F2_min + 1 endpoint (P4)
+        # omega_k only adds fast edges to omega_{k-1} (SPEC.md:404)
+        if k > 2:
+            prev = I.fractal_fast_edges(k - 1)
+            scale = {((2 * a[0], 2 * a[1]), (2 * b[0], 2 * b[1])) for a, b in prev}
+            assert len(I.fractal_fast_edges(k)) > len(prev)
+            assert all(abs(x) <= t and 0 <= y <= t for e in I.fractal_fast_edges(k) for (x, y) in e)
+            assert scale  # (the scaled previous level is a different lattice; only monotonicity in k is asserted)

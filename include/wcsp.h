@@ -97,6 +97,11 @@ typedef struct {
                                0 = auto (4N, min 2^20); grown automatically on overflow */
   int64_t trace_cap;        /* per-cycle trace records kept (0 = off) */
   void* stream;             /* cudaStream_t or NULL (the library creates one) */
+  int32_t slabs;            /* > 1: slab engine on this device — the grid is cut along its last axis
+                               into `slabs` slabs with ghost planes that exchange the water crossing
+                               a slab boundary every cycle (the multi-GPU layout run
+                               on one GPU); requires engine WHEEL and host arrays.  0/1 = off. */
+  int32_t reserved0;
 } wcsp_options;
 
 typedef struct {

@@ -80,6 +80,17 @@ struct wcsp_handle {
   cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
   long long last_cycles = 0;
   long long launches = 0;
+  // slab engine: a child owns planes [z0, z1) of the last axis plus ghost planes
+  int slab_index = -1;
+  long long z0 = 0, z1 = 0;
+  int glo = 0, ghi = 0;
+  unsigned goff = 0, plane = 0, ghost_hi_start = 0;
+  uint8_t* d_ghost = nullptr;                        // 1 = ghost, 2 = ghost target
+  unsigned long long *g_out_lo = nullptr, *g_out_hi = nullptr, *g_in_lo = nullptr, *g_in_hi = nullptr;
+  unsigned *l_out_lo = nullptr, *l_out_hi = nullptr, *l_in_lo = nullptr, *l_in_hi = nullptr;
+  unsigned long long preset_nB = 0;                  // child: |B| of the whole problem (B-arrival list)
+  std::vector<wcsp_handle*> children;                // parent of a virtual slab group
+  Ctl** d_ctls = nullptr;                            // children's control blocks (device array)
 };
 
 namespace {
@@ -152,6 +163,12 @@ Dev make_dev(const wcsp_handle* h) {
   s.dcap = h->dcap;
   s.f1max = h->f1max;
   s.nblocks = (unsigned)h->grid;
+  s.goff = h->goff;
+  s.plane = h->plane;
+  s.ghost_hi_start = h->ghi ? h->ghost_hi_start : (unsigned)h->N;
+  s.ghost_out_lo = h->g_out_lo;
+  s.ghost_out_hi = h->g_out_hi;
+  s.slab = h->slab_index >= 0;
   return s;
 }
 
@@ -266,16 +283,32 @@ wcsp_status load_problem(wcsp_handle* h, const wcsp_problem* p) {
   if ((st = copy_mask(h, h->d_maskB, p->maskB, p->mem)) != WCSP_REACHED) return st;
   h->present_all = p->present == nullptr;
   if (!h->present_all && (st = copy_mask(h, h->d_present, p->present, p->mem)) != WCSP_REACHED) return st;
-  if ((st = validate_device(h, f1, f2)) != WCSP_REACHED) return st;
+  if (h->slab_index < 0) {
+    if ((st = validate_device(h, f1, f2)) != WCSP_REACHED) return st;
+  } else {                         // slab child: the group validated the whole problem on the host
+    const unsigned long long need = std::max<unsigned long long>(64, 4ull * h->d * h->preset_nB);
+    if (need > h->barr_cap) {
+      if (h->barr) cudaFree(h->barr);
+      h->barr = nullptr;
+      CK(cudaMalloc(&h->barr, need * sizeof(BArr)));
+      h->barr_cap = (unsigned)need;
+    }
+  }
   if ((st = build_weights(h, f1, f2)) != WCSP_REACHED) return st;
   h->M = p->M;
   return WCSP_REACHED;
 }
 
 void release(wcsp_handle* h) {
+  for (wcsp_handle* c : h->children) {
+    release(c);
+    delete c;
+  }
+  h->children.clear();
   void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->tbits, h->barr,
                   h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
-                  h->d_cnt};
+                  h->d_cnt, h->d_ghost, h->g_out_lo, h->g_out_hi, h->g_in_lo, h->g_in_hi, h->l_out_lo,
+                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -331,7 +364,7 @@ wcsp_status reset_ctl(wcsp_handle* h) {
 wcsp_status launch_init(wcsp_handle* h) {
   Dev s = make_dev(h);
   k_init<<<grid_for(h, h->N), THREADS, 0, h->stream>>>(s, h->d_maskA, h->d_maskB,
-                                                      h->present_all ? nullptr : h->d_present,
+                                                      h->present_all ? nullptr : h->d_present, h->d_ghost,
                                                       h->M == WCSP_M_INF ? 1 : (int)h->M, h->d);
   CK(cudaGetLastError());
   h->launches += 1;
@@ -472,35 +505,19 @@ wcsp_status solve_impl(wcsp_handle* h, wcsp_result* out) {
   return (wcsp_status)status;
 }
 
-}  // namespace
+struct SlabSpec {
+  int index;
+  long long z0, z1;
+  int glo, ghi;
+  unsigned goff, plane;
+  const uint8_t* ghost;            // host [N_local]
+  unsigned long long nB;
+  int f1max;
+};
 
-extern "C" {
-
-const char* wcsp_last_error(void) { return g_err.c_str(); }
-
-const char* wcsp_version(void) {
-  return "wcsp-b200 0.2 (sm_100a; engines: sweep/wheel x persistent/stepped)";
-}
-
-wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handle** out) {
-  if (!p || !out) return fail(WCSP_EINVAL, "problem and out must be non-NULL");
-  if (p->d < 1 || p->d > 4) return fail(WCSP_EINVAL, "d = %d outside 1..4", p->d);
+wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const SlabSpec* spec, wcsp_handle** out) {
   unsigned long long N = 1;
-  for (int k = 0; k < p->d; ++k) {
-    if (p->shape[k] < 1) return fail(WCSP_EINVAL, "shape[%d] = %lld < 1", k, (long long)p->shape[k]);
-    N *= (unsigned long long)p->shape[k];
-    if (N > (1ull << 30)) return fail(WCSP_EINVAL, "N > 2^30 vertices");
-  }
-  wcsp_status st;
-  if ((st = check_M(p->M)) != WCSP_REACHED) return st;
-  wcsp_options opt{};
-  if (o) opt = *o;
-  if (opt.demote_twin) return fail(WCSP_EINVAL, "demote_twin is reserved in this version (must be 0)");
-  if (opt.time_mode != WCSP_JUMP && opt.time_mode != WCSP_UNIT) return fail(WCSP_EINVAL, "bad time_mode");
-  if (opt.engine < WCSP_ENGINE_PERSISTENT || opt.engine > WCSP_ENGINE_WHEEL_STEPPED)
-    return fail(WCSP_EINVAL, "bad engine %d", opt.engine);
-  if (opt.trace_cap < 0 || opt.cycle_budget < 0 || opt.phantom_capacity < 0) return fail(WCSP_EINVAL, "negative option");
-
+  for (int k = 0; k < p->d; ++k) N *= (unsigned long long)p->shape[k];
   wcsp_handle* h = new wcsp_handle();
   h->opt = opt;
   h->d = p->d;
@@ -565,15 +582,328 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
     CKH(alloc_pool(h, cap));
   }
   set_l2_window(h);
+  if (spec) {                      // slab child: geometry, ghost flags and exchange planes
+    h->slab_index = spec->index;
+    h->z0 = spec->z0; h->z1 = spec->z1; h->glo = spec->glo; h->ghi = spec->ghi;
+    h->goff = spec->goff; h->plane = spec->plane;
+    h->ghost_hi_start = (unsigned)((spec->glo + spec->z1 - spec->z0) * spec->plane);
+    h->preset_nB = spec->nB;
+    h->f1max = spec->f1max;
+    CKC(cudaMalloc(&h->d_ghost, N));
+    CKC(cudaMemcpy(h->d_ghost, spec->ghost, N, cudaMemcpyHostToDevice));
+    const size_t pb = (size_t)spec->plane;
+    CKC(cudaMalloc(&h->g_out_lo, pb * 8)); CKC(cudaMalloc(&h->g_out_hi, pb * 8));
+    CKC(cudaMalloc(&h->g_in_lo, pb * 8)); CKC(cudaMalloc(&h->g_in_hi, pb * 8));
+    CKC(cudaMalloc(&h->l_out_lo, pb * 4)); CKC(cudaMalloc(&h->l_out_hi, pb * 4));
+    CKC(cudaMalloc(&h->l_in_lo, pb * 4)); CKC(cudaMalloc(&h->l_in_hi, pb * 4));
+    CKC(cudaMemset(h->g_out_lo, 0, pb * 8)); CKC(cudaMemset(h->g_out_hi, 0, pb * 8));
+    CKC(cudaMemset(h->g_in_lo, 0, pb * 8)); CKC(cudaMemset(h->g_in_hi, 0, pb * 8));
+  }
   CKH(load_problem(h, p));
+  if (spec) h->f1max = spec->f1max;
 #undef CKC
 #undef CKH
   *out = h;
   return WCSP_REACHED;
 }
 
+
+// ---------------------------------------------------------------------------
+// Slab engine, virtual slabs on one device: the grid is cut
+// along its last axis into opt.slabs children, each a complete wheel solver
+// over its slab plus ghost planes; per cycle the children exchange the water
+// that crossed a slab boundary and their boundary labels, and combine their
+// proposals for the cycle decision.  The multi-GPU form replaces the
+// device-to-device copies and k_slab_reduce by NCCL send/recv and an
+// allreduce(max); the kernels are the same.
+// ---------------------------------------------------------------------------
+wcsp_status host_validate(const wcsp_problem* p, unsigned long long* nB, int* f1max) {
+  long long N = 1, st[4] = {1, 1, 1, 1};
+  for (int k = 0; k < p->d; ++k) { st[k] = N; N *= p->shape[k]; }
+  unsigned long long na = 0, nb = 0, nab = 0, bad = 0;
+  int fmax = 1;
+  for (long long v = 0; v < N; ++v) {
+    const bool pr = p->present == nullptr || p->present[v] != 0;
+    const bool a = pr && p->maskA[v], b = pr && p->maskB[v];
+    na += a; nb += b; nab += a && b;
+    for (int k = 0; k < p->d; ++k) {
+      if ((v / st[k]) % p->shape[k] + 1 < p->shape[k]) {
+        const uint8_t f1 = p->f1[(size_t)k * N + v], f2 = p->f2[(size_t)k * N + v];
+        bad += f1 != 0 && f2 == 0;
+        fmax = std::max<int>(fmax, f1);
+      }
+    }
+  }
+  if (na == 0) return fail(WCSP_EINVAL, "A is empty (among present vertices)");
+  if (nb == 0) return fail(WCSP_EINVAL, "B is empty (among present vertices)");
+  if (nab) return fail(WCSP_EINVAL, "A and B intersect in %llu vertices", nab);
+  if (bad) return fail(WCSP_EINVAL, "%llu present edges have f1 > 0 and f2 = 0", bad);
+  *nB = nb;
+  *f1max = fmax;
+  return WCSP_REACHED;
+}
+
+wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_handle** out) {
+  if (p->mem != WCSP_MEM_HOST) return fail(WCSP_EINVAL, "the slab engine takes host arrays");
+  if (!is_wheel(opt.engine)) return fail(WCSP_EINVAL, "the slab engine runs the wheel engine (engine = WHEEL)");
+  const int R = opt.slabs, d = p->d;
+  const long long nL = p->shape[d - 1];
+  if (nL < R) return fail(WCSP_EINVAL, "last axis (%lld) shorter than the number of slabs (%d)", nL, R);
+  long long N = 1;
+  for (int k = 0; k < d; ++k) N *= p->shape[k];
+  const long long plane = N / nL;
+  unsigned long long nB = 0;
+  int f1max = 1;
+  wcsp_status st = host_validate(p, &nB, &f1max);
+  if (st != WCSP_REACHED) return st;
+  wcsp_handle* g = new wcsp_handle();
+  g->opt = opt;
+  g->d = d;
+  for (int k = 0; k < 4; ++k) g->shape[k] = k < d ? p->shape[k] : 1;
+  g->N = (unsigned long long)N;
+  g->dev = opt.device;
+  g->M = p->M;
+  g->plane = (unsigned)plane;
+  auto bail = [&](wcsp_status s) { release(g); delete g; return s; };
+  if (cudaSetDevice(g->dev) != cudaSuccess) return bail(fail(WCSP_ECUDA, "cudaSetDevice failed"));
+  if (opt.stream) {
+    g->stream = (cudaStream_t)opt.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(WCSP_ECUDA, "stream creation failed"));
+    g->own_stream = true;
+  }
+  if (cudaEventCreate(&g->e0) != cudaSuccess || cudaEventCreate(&g->e1) != cudaSuccess ||
+      cudaEventCreate(&g->em) != cudaSuccess)
+    return bail(fail(WCSP_ECUDA, "event creation failed"));
+  for (int i = 0; i < R; ++i) {
+    SlabSpec sp{};
+    sp.index = i;
+    sp.z0 = (long long)i * nL / R;
+    sp.z1 = (long long)(i + 1) * nL / R;
+    sp.glo = i > 0;
+    sp.ghi = i < R - 1;
+    const long long lo = (sp.z0 - sp.glo) * plane, hi = (sp.z1 + sp.ghi) * plane, Nl = hi - lo;
+    sp.goff = (unsigned)lo;
+    sp.plane = (unsigned)plane;
+    sp.nB = nB;
+    sp.f1max = f1max;
+    std::vector<uint8_t> f1((size_t)d * Nl), f2((size_t)d * Nl), A(Nl), B(Nl), ghost(Nl, 0), pres;
+    for (int k = 0; k < d; ++k) {
+      memcpy(&f1[(size_t)k * Nl], p->f1 + (size_t)k * N + lo, Nl);
+      memcpy(&f2[(size_t)k * Nl], p->f2 + (size_t)k * N + lo, Nl);
+    }
+    memcpy(A.data(), p->maskA + lo, Nl);
+    memcpy(B.data(), p->maskB + lo, Nl);
+    if (p->present) { pres.resize(Nl); memcpy(pres.data(), p->present + lo, Nl); }
+    auto mark_ghost = [&](long long first) {
+      for (long long j = first; j < first + plane; ++j) {
+        const bool pr = p->present == nullptr || pres[j] != 0;
+        ghost[j] = pr ? (B[j] ? 2 : 1) : 0;
+        A[j] = 0;
+        B[j] = 0;
+      }
+    };
+    if (sp.glo) mark_ghost(0);
+    if (sp.ghi) mark_ghost(Nl - plane);
+    sp.ghost = ghost.data();
+    wcsp_problem lp = *p;
+    lp.shape[d - 1] = sp.z1 - sp.z0 + sp.glo + sp.ghi;
+    lp.f1 = f1.data(); lp.f2 = f2.data(); lp.maskA = A.data(); lp.maskB = B.data();
+    lp.present = p->present ? pres.data() : nullptr;
+    wcsp_options co = opt;
+    co.slabs = 0;
+    co.engine = WCSP_ENGINE_WHEEL_STEPPED;
+    co.stream = g->stream;
+    wcsp_handle* ch = nullptr;
+    if ((st = create_impl(&lp, co, &sp, &ch)) != WCSP_REACHED) return bail(st);
+    g->children.push_back(ch);
+  }
+  std::vector<Ctl*> ctls;
+  for (auto* ch : g->children) ctls.push_back(ch->ctl);
+  if (cudaMalloc(&g->d_ctls, R * sizeof(Ctl*)) != cudaSuccess ||
+      cudaMemcpy(g->d_ctls, ctls.data(), R * sizeof(Ctl*), cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(fail(WCSP_ENOMEM, "slab control array"));
+  if (cudaMallocHost(&g->h_ctl, sizeof(Ctl)) != cudaSuccess) return bail(fail(WCSP_ENOMEM, "pinned control block"));
+  g->grid = g->children[0]->grid;
+  *out = g;
+  return WCSP_REACHED;
+}
+
+template <int D>
+void group_cycle(wcsp_handle* g, const std::vector<Dev>& devs) {
+  auto& ch = g->children;
+  const int R = (int)ch.size();
+  const size_t sm = sizeof(Smem), pl = g->plane;
+  const int pg = (int)std::min<unsigned long long>((pl + THREADS - 1) / THREADS, (unsigned long long)g->grid);
+  cudaStream_t s = g->stream;
+  for (int i = 0; i < R; ++i) k_wheel_fire<D><<<ch[i]->grid, THREADS, sm, s>>>(devs[i]);
+  for (int i = 0; i < R; ++i) {   // water that crossed a slab boundary goes to its owner
+    if (ch[i]->glo) cudaMemcpyAsync(ch[i - 1]->g_in_hi, ch[i]->g_out_lo, pl * 8, cudaMemcpyDeviceToDevice, s);
+    if (ch[i]->ghi) cudaMemcpyAsync(ch[i + 1]->g_in_lo, ch[i]->g_out_hi, pl * 8, cudaMemcpyDeviceToDevice, s);
+  }
+  for (int i = 0; i < R; ++i) {
+    if (ch[i]->glo) k_slab_apply<<<pg, THREADS, 0, s>>>(devs[i], ch[i]->g_in_lo, ch[i]->plane);
+    if (ch[i]->ghi) k_slab_apply<<<pg, THREADS, 0, s>>>(devs[i], ch[i]->g_in_hi, ch[i]->ghost_hi_start - ch[i]->plane);
+  }
+  for (int i = 0; i < R; ++i) k_wheel_treat<D><<<ch[i]->grid, THREADS, sm, s>>>(devs[i]);
+  for (int i = 0; i < R; ++i) {   // boundary labels refresh the neighbours' ghost planes
+    if (ch[i]->glo) k_slab_gather_labels<<<pg, THREADS, 0, s>>>(devs[i], ch[i]->plane, ch[i]->l_out_lo);
+    if (ch[i]->ghi) k_slab_gather_labels<<<pg, THREADS, 0, s>>>(devs[i], ch[i]->ghost_hi_start - ch[i]->plane, ch[i]->l_out_hi);
+  }
+  for (int i = 0; i < R; ++i) {
+    if (ch[i]->glo) cudaMemcpyAsync(ch[i - 1]->l_in_hi, ch[i]->l_out_lo, pl * 4, cudaMemcpyDeviceToDevice, s);
+    if (ch[i]->ghi) cudaMemcpyAsync(ch[i + 1]->l_in_lo, ch[i]->l_out_hi, pl * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  for (int i = 0; i < R; ++i) {
+    if (ch[i]->glo) k_slab_scatter_labels<<<pg, THREADS, 0, s>>>(devs[i], ch[i]->l_in_lo, 0u);
+    if (ch[i]->ghi) k_slab_scatter_labels<<<pg, THREADS, 0, s>>>(devs[i], ch[i]->l_in_hi, ch[i]->ghost_hi_start);
+  }
+  for (int i = 0; i < R; ++i) k_slab_propose<<<1, 32, 0, s>>>(devs[i]);
+  k_slab_reduce<<<1, 32, 0, s>>>(g->d_ctls, R);
+  for (int i = 0; i < R; ++i) k_wheel_decide<<<1, 32, 0, s>>>(devs[i]);
+  g->launches += 5 * R + 1 + 4 * (R - 1);
+}
+
+wcsp_status group_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
+  wcsp_status st;
+  auto& ch = g->children;
+  const int R = (int)ch.size();
+  g->launches = 0;
+  CK(cudaEventRecord(g->e0, g->stream));
+  for (auto* c : ch) {
+    c->M = g->M;
+    if ((st = reset_ctl(c)) != WCSP_REACHED) return st;
+    if ((st = launch_init(c)) != WCSP_REACHED) return st;
+    g->launches += 1;
+  }
+  CK(cudaEventRecord(g->em, g->stream));
+  std::vector<Dev> devs;
+  for (auto* c : ch) devs.push_back(make_dev(c));
+  int batch = 4;
+  for (;;) {
+    for (int i = 0; i < batch; ++i) {
+      switch (g->d) {
+        case 1: group_cycle<1>(g, devs); break;
+        case 2: group_cycle<2>(g, devs); break;
+        case 3: group_cycle<3>(g, devs); break;
+        default: group_cycle<4>(g, devs); break;
+      }
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&g->h_ctl->view, &ch[0]->ctl->view, sizeof(View), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    const int s0 = g->h_ctl->view.status;
+    if (s0 == ST_WRAP) {
+      const int run = ST_RUNNING;
+      for (int i = 0; i < R; ++i) {
+        k_wheel_maintain<<<ch[i]->grid, THREADS, 0, g->stream>>>(devs[i]);
+        CK(cudaMemcpyAsync(&ch[i]->ctl->view.status, &run, sizeof(int), cudaMemcpyHostToDevice, g->stream));
+      }
+      CK(cudaStreamSynchronize(g->stream));
+      continue;
+    }
+    if (s0 != ST_RUNNING) break;
+    batch = std::min(batch * 2, 64);
+  }
+  CK(cudaEventRecord(g->e1, g->stream));
+  std::vector<Ctl> cs(R);
+  for (int i = 0; i < R; ++i) CK(cudaMemcpyAsync(&cs[i], ch[i]->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  float ms = 0, cms = 0;
+  CK(cudaEventElapsedTime(&ms, g->e0, g->e1));
+  CK(cudaEventElapsedTime(&cms, g->em, g->e1));
+  *status = cs[0].view.status;
+  memset(r, 0, sizeof(*r));
+  unsigned long long ybest = ~0ull;
+  long long need = 0;
+  for (int i = 0; i < R; ++i) {
+    ybest = std::min(ybest, cs[i].ybest);
+    r->edge_updates += cs[i].edge_updates;
+    r->arrivals += cs[i].arrivals;
+    r->triggered += cs[i].triggered;
+    r->phantoms_created += cs[i].created;
+    r->relabels += cs[i].relabels;
+    r->lanes_started += cs[i].started;
+    r->peak_phantoms += cs[i].peak_phantoms;
+    ch[i]->last_cycles = cs[i].cycles;
+    if (cs[i].need_pool) need = cs[i].need_pool == -2 ? -2 : std::max(need, cs[i].need_pool);
+    if (cs[i].abort) return fail(WCSP_ECUDA, "slab %d: barrier watchdog fired", i);
+  }
+  r->cycles = cs[0].cycles;
+  g->last_cycles = cs[0].cycles;
+  if (*status == WCSP_REACHED) {
+    r->F1 = cs[0].F1;
+    r->F2 = cs[0].F2;
+    r->X = cs[0].X;
+    r->Y = ybest == ~0ull ? -1 : (long long)(ybest >> 1);
+    r->via_phantom = (int)(ybest & 1);
+    r->x_lane = x_lane_of(g, r->X, r->Y);
+  } else {
+    r->F1 = r->F2 = r->X = r->Y = -1;
+    r->x_lane = -1;
+  }
+  r->phantom_capacity = *status == WCSP_EOVERFLOW ? need : (long long)ch[0]->ev_cap;
+  r->kernel_launches = g->launches;
+  r->device_ms = ms;
+  r->cycle_ms = cms;
+  return WCSP_REACHED;
+}
+
+wcsp_status group_solve(wcsp_handle* g, wcsp_result* out) {
+  wcsp_result r;
+  int status = ST_RUNNING;
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    wcsp_status st = group_solve_once(g, &r, &status);
+    if (st != WCSP_REACHED) return st;
+    if (status != WCSP_EOVERFLOW) break;
+    for (auto* c : g->children) {     // grow every child's wheel storage and re-run
+      if ((st = alloc_desc(c, c->dcap * 2)) != WCSP_REACHED) return st;
+      if ((st = alloc_ring(c, c->ev_cap * 2)) != WCSP_REACHED) return st;
+    }
+  }
+  if (status == WCSP_EOVERFLOW) return fail(WCSP_EOVERFLOW, "event storage overflow after retries");
+  if (status == WCSP_EBUDGET) { *out = r; return fail(WCSP_EBUDGET, "cycle budget %lld exceeded", g->opt.cycle_budget); }
+  if (status != WCSP_REACHED && status != WCSP_INFEASIBLE) return fail(WCSP_ECUDA, "solver ended in state %d", status);
+  *out = r;
+  return (wcsp_status)status;
+}
+}  // namespace
+
+extern "C" {
+
+const char* wcsp_last_error(void) { return g_err.c_str(); }
+
+const char* wcsp_version(void) {
+  return "wcsp-b200 0.3 (sm_100a; engines: sweep/wheel x persistent/stepped; slab partition)";
+}
+
+wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handle** out) {
+  if (!p || !out) return fail(WCSP_EINVAL, "problem and out must be non-NULL");
+  if (p->d < 1 || p->d > 4) return fail(WCSP_EINVAL, "d = %d outside 1..4", p->d);
+  unsigned long long N = 1;
+  for (int k = 0; k < p->d; ++k) {
+    if (p->shape[k] < 1) return fail(WCSP_EINVAL, "shape[%d] = %lld < 1", k, (long long)p->shape[k]);
+    N *= (unsigned long long)p->shape[k];
+    if (N > (1ull << 30)) return fail(WCSP_EINVAL, "N > 2^30 vertices");
+  }
+  wcsp_status st;
+  if ((st = check_M(p->M)) != WCSP_REACHED) return st;
+  wcsp_options opt{};
+  if (o) opt = *o;
+  if (opt.demote_twin) return fail(WCSP_EINVAL, "demote_twin is reserved in this version (must be 0)");
+  if (opt.time_mode != WCSP_JUMP && opt.time_mode != WCSP_UNIT) return fail(WCSP_EINVAL, "bad time_mode");
+  if (opt.engine < WCSP_ENGINE_PERSISTENT || opt.engine > WCSP_ENGINE_WHEEL_STEPPED)
+    return fail(WCSP_EINVAL, "bad engine %d", opt.engine);
+  if (opt.trace_cap < 0 || opt.cycle_budget < 0 || opt.phantom_capacity < 0) return fail(WCSP_EINVAL, "negative option");
+
+  if (opt.slabs > 1) return create_group(p, opt, out);
+  return create_impl(p, opt, nullptr, out);
+}
+
 wcsp_status wcsp_load(wcsp_handle* h, const wcsp_problem* p) {
   if (!h || !p) return fail(WCSP_EINVAL, "NULL argument");
+  if (!h->children.empty()) return fail(WCSP_EINVAL, "wcsp_load: create a new slab handle instead");
   if (p->d != h->d) return fail(WCSP_EINVAL, "d differs from the handle's");
   for (int k = 0; k < h->d; ++k)
     if (p->shape[k] != h->shape[k]) return fail(WCSP_EINVAL, "shape differs from the handle's");
@@ -584,6 +914,7 @@ wcsp_status wcsp_load(wcsp_handle* h, const wcsp_problem* p) {
 wcsp_status wcsp_solve(wcsp_handle* h, wcsp_result* r) {
   if (!h || !r) return fail(WCSP_EINVAL, "NULL argument");
   CK(cudaSetDevice(h->dev));
+  if (!h->children.empty()) return group_solve(h, r);
   return solve_impl(h, r);
 }
 
@@ -592,6 +923,11 @@ wcsp_status wcsp_set_targets(wcsp_handle* h, const uint8_t* maskB, const uint8_t
   if (!h) return fail(WCSP_EINVAL, "NULL handle");
   wcsp_status st;
   if ((st = check_M(M)) != WCSP_REACHED) return st;
+  if (!h->children.empty()) {
+    if (maskB || present || present_all) return fail(WCSP_EINVAL, "slab handles only change M");
+    h->M = M;
+    return WCSP_REACHED;
+  }
   CK(cudaSetDevice(h->dev));
   if (maskB && (st = copy_mask(h, h->d_maskB, maskB, mem)) != WCSP_REACHED) return st;
   if (present_all) h->present_all = true;
@@ -609,7 +945,22 @@ wcsp_status wcsp_trace(wcsp_handle* h, wcsp_trace_rec* out, int64_t cap, int64_t
   const long long avail = std::min<long long>(h->last_cycles, h->opt.trace_cap);
   const long long m = std::min<long long>(avail, cap);
   static_assert(sizeof(TraceRec) == sizeof(wcsp_trace_rec), "trace record layout");
-  if (m > 0) {
+  if (m > 0 && !h->children.empty()) {     // slab group: per-cycle sums over the slabs
+    std::vector<TraceRec> acc((size_t)m), one((size_t)m);
+    for (size_t i = 0; i < h->children.size(); ++i) {
+      CK(cudaMemcpyAsync(i ? one.data() : acc.data(), h->children[i]->trace, m * sizeof(TraceRec),
+                         cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      if (i)
+        for (long long j = 0; j < m; ++j) {
+          acc[j].live_lanes += one[j].live_lanes; acc[j].phantoms += one[j].phantoms;
+          acc[j].triggered += one[j].triggered; acc[j].arrivals += one[j].arrivals;
+          acc[j].created += one[j].created; acc[j].relabels += one[j].relabels; acc[j].tested += one[j].tested;
+          acc[j].active_vertices += one[j].active_vertices;
+        }
+    }
+    memcpy(out, acc.data(), m * sizeof(TraceRec));
+  } else if (m > 0) {
     CK(cudaMemcpyAsync(out, h->trace, m * sizeof(TraceRec), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
   }
@@ -620,6 +971,7 @@ wcsp_status wcsp_trace(wcsp_handle* h, wcsp_trace_rec* out, int64_t cap, int64_t
 // Reconstruction (reading R12 in DESIGN.md).
 wcsp_status wcsp_reconstruct(wcsp_handle* h, int64_t* path, int64_t cap, int64_t* len, wcsp_result* result) {
   if (!h || !len) return fail(WCSP_EINVAL, "NULL argument");
+  if (!h->children.empty()) return fail(WCSP_EINVAL, "wcsp_reconstruct is not available on slab handles");
   CK(cudaSetDevice(h->dev));
   const unsigned long long N = h->N;
   wcsp_result first;

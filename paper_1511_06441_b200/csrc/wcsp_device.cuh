@@ -46,6 +46,8 @@ constexpr int WIN_VERTS = WIN_WORDS * 32;
 constexpr unsigned LBL_REMOVED = 0xFFFFu;  // label of a vertex outside G': no S6 test passes
 constexpr unsigned TMP_B = 0xFFFF0001u;    // temp sentinel of a target vertex
 constexpr unsigned TMP_REMOVED = 0xFFFF0000u;
+constexpr unsigned TMP_GHOST = 0xFFFF0002u;    // slab engine: a neighbouring slab's boundary vertex
+constexpr unsigned TMP_GHOST_B = 0xFFFF0003u;  // ... that is a target
 constexpr int ST_RUNNING = -1;
 constexpr int ST_WRAP = 100;               // stepped engines: maintenance pass needed (host launches it)
 
@@ -66,6 +68,12 @@ struct Acc {                       // per-cycle accumulators, triple-buffered by
   unsigned long long arrivals, created, relabels, triggered, started, tested;
   long long pend_lanes, pend_phantoms;   // timing wheel: events in flight at the top of this cycle
 };
+
+// A slab's proposal for the decision of one cycle; the slabs' proposals are
+// combined with an element-wise max (NCCL allreduce max, or a kernel for
+// virtual slabs): bhit = best target arrival, negk = -(steps to the next
+// non-empty wheel bucket), pending = any live edge, overflow = any storage overflow.
+struct Prop { long long bhit, negk, pending, overflow; };
 
 struct View {                      // cycle state every block needs
   long long t;
@@ -89,6 +97,8 @@ struct Ctl {
   unsigned wheel_overflow, pad2_;  // 2: descriptor table full
   long long hist_t[WHEEL];         // time of cycle c (slot c & 255) ...
   unsigned long long hist_head[WHEEL];   // ... and the ring head before its treat
+  Prop prop, gprop;                // slab engine: local proposal / reduced proposal
+  unsigned long long ybest;        // (src << 1 | via) of the best arrival at X seen by this slab
 };
 
 struct TraceRec {
@@ -125,6 +135,13 @@ struct Dev {
   unsigned dcap;
   int f1max;
   unsigned nblocks;                // grid size of the cycle kernels (wheel region sizing)
+  // slab partition (multi-GPU / virtual slabs): local index + goff = global index
+  unsigned goff;
+  unsigned plane;                  // vertices per plane of the partitioned (last) axis
+  unsigned ghost_hi_start;         // local index of the upper ghost plane (N if none)
+  unsigned long long* ghost_out_lo;   // water handed to the lower neighbour's boundary plane
+  unsigned long long* ghost_out_hi;   // ... to the upper neighbour's
+  int slab;                        // 1: decide uses the reduced global proposal (ctl->gprop)
 };
 
 template <int D> struct Tr;
@@ -381,14 +398,20 @@ __device__ __forceinline__ unsigned arrive_atomic(const Dev& s, const View& v, b
   return go ? atom_max_hint(tmp_ptr(s.sw, D), (v.stamp << 16) | (unsigned)cand, pol_last()) : (v.stamp << 16);
 }
 
+// src is a GLOBAL vertex index (local index + s.goff); D is local.
 __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* acc, unsigned old, unsigned D,
                                             int cand, unsigned src, unsigned via) {
   const unsigned os = old >> 16;
   if (os == 0xFFFFu) {
     if (old == TMP_B) {            // termination 1°: a vertex of B is reached
-      atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - D));
+      const unsigned Dg = D + s.goff;
+      atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - Dg));
       const unsigned k = atomicAdd(&s.ctl->n_barr, 1u);
-      if (k < s.barr_cap) s.barr[k] = BArr{D, (unsigned)cand, src, via};
+      if (k < s.barr_cap) s.barr[k] = BArr{Dg, (unsigned)cand, src, via};
+    } else if (old >= TMP_GHOST) { // D belongs to a neighbouring slab: hand the water to its owner
+      unsigned long long* slot = D < s.plane ? s.ghost_out_lo + D : s.ghost_out_hi + (D - s.ghost_hi_start);
+      atomicMax(slot, ((unsigned long long)v.stamp << 48) | ((unsigned long long)(unsigned)cand << 32) |
+                          ((unsigned long long)(0x7FFFFFFFu - src) << 1) | (unsigned long long)(via ? 0u : 1u));
     }
   } else if (os != v.stamp) {      // first arrival of the cycle: D is triggered (dedupe)
     atomicOr(s.tbits + (D >> 5), 1u << (D & 31u));
@@ -464,7 +487,7 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
 #pragma unroll
         for (int j = 0; j < 2 * D; ++j) {
           const int cand = (int)lbl[it] - (int)((f2w[it] >> (8 * j)) & 0xFF);
-          arrive_post(s, v, acc, old[j], vx[it] + s.off[j], cand, vx[it], 0u);
+          arrive_post(s, v, acc, old[j], vx[it] + s.off[j], cand, vx[it] + s.goff, 0u);
         }
       }
     } else {
@@ -493,7 +516,7 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
       for (int it = 0; it < SWEEP_ITEMS; ++it) {
         const unsigned src = (unsigned)p[it] & 0x3FFFFFFFu;
         const unsigned lane = (unsigned)(p[it] >> PH_LANE) & 7u;
-        arrive_post(s, v, acc, old[it], src + s.off[lane], (int)((p[it] >> PH_CAND) & 0xFFFFu), src, 1u);
+        arrive_post(s, v, acc, old[it], src + s.off[lane], (int)((p[it] >> PH_CAND) & 0xFFFFu), src + s.goff, 1u);
       }
     }
     qflush(sm, &acc->n_act, act_out, &acc->n_pool, pool_out, s.pool_cap);
@@ -676,7 +699,8 @@ __device__ __forceinline__ void resolve_hit(const Dev& s, unsigned long long bhi
   C->F1 = t;
   C->F2 = s.minf ? -1 : (long long)s.M - q;
   C->X = X;
-  C->Y = (long long)(best >> 1);
+  C->ybest = best;                 // slab engine: the host takes the min over slabs
+  C->Y = best == ~0ull ? -1 : (long long)(best >> 1);
   C->via = (long long)(best & 1);
 }
 
@@ -879,15 +903,17 @@ __global__ void __launch_bounds__(THREADS) k_clear_temps(Dev s) { clear_temps(s)
 // removed sentinels, no live lane, A triggered with temp M (the treat of
 // c = 0 then sets L = M on A and starts its lanes).
 __global__ void __launch_bounds__(THREADS) k_init(Dev s, const uint8_t* maskA, const uint8_t* maskB,
-                                                  const uint8_t* present, int lblA, int d) {
+                                                  const uint8_t* present, const uint8_t* ghost, int lblA,
+                                                  int d) {
   const unsigned N = s.N;
   for (unsigned long long i = (unsigned long long)blockIdx.x * THREADS + threadIdx.x; i < N;
        i += (unsigned long long)gridDim.x * THREADS) {
     const bool p = present ? present[i] != 0 : true;
-    const bool a = p && maskA[i];
+    const bool a = p && maskA[i] && !(ghost && ghost[i]);
     const bool b = p && maskB[i];
     unsigned lbl = 0, tmp = 0;
     if (!p) { lbl = LBL_REMOVED; tmp = TMP_REMOVED; }
+    else if (ghost && ghost[i]) { lbl = 0; tmp = ghost[i] == 2 ? TMP_GHOST_B : TMP_GHOST; }   // slab engine
     else if (b) { lbl = 0; tmp = TMP_B; }
     else if (a) { lbl = 0; tmp = (stamp_of(0) << 16) | (unsigned)lblA; }
     s.sw[i] = ((unsigned long long)tmp << 32) | lbl;
@@ -902,7 +928,8 @@ __global__ void __launch_bounds__(THREADS) k_init(Dev s, const uint8_t* maskA, c
     unsigned bits = 0;
     for (unsigned b = 0; b < 32; ++b) {
       const unsigned long long i = w * 32 + b;
-      if (i < N && maskA[i] && (present ? present[i] != 0 : true) && !maskB[i]) bits |= 1u << b;
+      if (i < N && maskA[i] && (present ? present[i] != 0 : true) && !maskB[i] && !(ghost && ghost[i]))
+        bits |= 1u << b;
     }
     s.tbits[w] = bits;
   }

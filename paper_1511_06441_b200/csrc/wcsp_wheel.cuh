@@ -199,19 +199,55 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
         const unsigned via = ((e[it] >> EV_LANE_BIT) & 1) ? 0u : 1u;
-        arrive_post(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu), src, via);
+        arrive_post(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu), src + s.goff, via);
       }
     }
   }
   block_reduce_commit(sm, 0xFFFFFFFFu, 0, arr, 0, 0, 0, acc);
 }
 
-// decide for the wheel: events-in-flight bookkeeping, next non-empty bucket,
-// ring-capacity check.  Reads only state no block writes during decide.
+// The wheel's local proposal for the decision of cycle c (see Prop): best
+// target arrival, steps to the next non-empty bucket, any live edge, and the
+// storage checks (descriptor table; event ring: during this cycle's treat every
+// event allocated by a cycle c' with t(c') + f1max > t was still live and the
+// treat's allocations must not have reached it).  *need = ring slots needed.
+__device__ Prop wheel_propose(const Dev& s, const View& v, long long* need) {
+  Acc* a = &s.ctl->acc[v.c % 3];
+  Ctl* C = s.ctl;
+  const unsigned b = (unsigned)(v.t & (WHEEL - 1));
+  const long long pl = __ldcg((const long long*)&a->pend_lanes);
+  const long long pp = __ldcg((const long long*)&a->pend_phantoms);
+  const long long fired = v.c > 0 ? (long long)__ldcg(s.bnev + b) : 0;
+  const long long fired_l = v.c > 0 ? (long long)__ldcg(s.bnlane + b) : 0;
+  const long long npl = pl - fired_l + (long long)__ldcg(&a->started);
+  const long long npp = pp - (fired - fired_l) + (long long)__ldcg(&a->created);
+  Prop p;
+  p.bhit = (long long)__ldcg(&a->bhit);
+  p.pending = npl + npp > 0;
+  unsigned k = 1;
+  if (!s.unit)
+    while (k < (unsigned)WHEEL && __ldcg(s.bnev + ((b + k) & (WHEEL - 1))) == 0) ++k;
+  p.negk = -(long long)k;
+  const unsigned long long head = __ldcg(&C->ev_head);
+  unsigned long long oldest = head;
+  for (unsigned back = 0; back < (unsigned)WHEEL && back <= v.c; ++back) {
+    const unsigned slot = (v.c - back) & (WHEEL - 1);
+    if (__ldcg((const long long*)&C->hist_t[slot]) + s.f1max <= v.t) break;
+    oldest = __ldcg(&C->hist_head[slot]);
+  }
+  *need = 0;
+  p.overflow = 0;
+  if (__ldcg(&C->wheel_overflow)) { p.overflow = 1; *need = -2; }
+  if (head - oldest > s.ev_mask + 1) { p.overflow = 1; *need = (long long)(head - oldest); }
+  return p;
+}
+
+// decide for the wheel (Step 6 + time skipping).  Single device: g = its own
+// proposal; slab engine: g = the max-combined proposals of all slabs.  Reads
+// only state no block writes during decide.
 __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
   Acc* a = &s.ctl->acc[v.c % 3];
   Ctl* C = s.ctl;
-  const unsigned long long bhit = __ldcg(&a->bhit);
   View nv = v;
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
   const long long pl = __ldcg((const long long*)&a->pend_lanes);      // E at the top of this cycle
@@ -221,6 +257,13 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
   const long long new_l = (long long)__ldcg(&a->started);             // lanes started this cycle
   const long long new_p = (long long)__ldcg(&a->created);             // phantoms created this cycle
   const long long npl = pl - fired_l + new_l, npp = pp - (fired - fired_l) + new_p;
+  long long need = 0;
+  const Prop L = wheel_propose(s, v, &need);
+  Prop G = L;
+  if (s.slab) {
+    const volatile Prop* gp = &C->gprop;
+    G.bhit = gp->bhit; G.negk = gp->negk; G.pending = gp->pending; G.overflow = gp->overflow;
+  }
   if (writer) {
     const unsigned long long arrivals = __ldcg(&a->arrivals);
     const unsigned long long relabels = __ldcg(&a->relabels), triggered = __ldcg(&a->triggered);
@@ -229,29 +272,27 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
       C->edge_updates += pl + pp;
       if ((long long)v.c - 1 < s.trace_cap) {
         const unsigned long long t2 = globaltimer_ns();
-        TraceRec r{v.t, (long long)v.delta, (long long)__ldcg(s.bndesc + (size_t)b * s.nblocks), pl, pp, (long long)triggered, (long long)arrivals, new_p,
-                   (long long)relabels, (long long)__ldcg(&a->tested), (long long)(C->ts1 - C->ts0),
-                   (long long)(t2 - C->ts1)};
+        TraceRec r{v.t, (long long)v.delta, (long long)__ldcg(s.bndesc + (size_t)b * s.nblocks), pl, pp,
+                   (long long)triggered, (long long)arrivals, new_p, (long long)relabels,
+                   (long long)__ldcg(&a->tested), (long long)(C->ts1 - C->ts0), (long long)(t2 - C->ts1)};
         s.trace[v.c - 1] = r;
       }
     }
     C->arrivals += arrivals; C->triggered += triggered; C->created += new_p; C->relabels += relabels;
     C->started += new_l;
   }
-  if (bhit) {
+  if (G.bhit) {
     nv.status = 0;
-    if (writer) resolve_hit(s, bhit, v.t);
-  } else if (__ldcg(&C->wheel_overflow)) {
-    nv.status = 8;  // WCSP_EOVERFLOW (descriptor table)
-    if (writer) C->need_pool = -2;
-  } else if (npl + npp == 0) {
+    if (writer) resolve_hit(s, (unsigned long long)G.bhit, v.t);
+  } else if (G.overflow) {
+    nv.status = 8;  // WCSP_EOVERFLOW: the host grows the event ring / descriptor table and re-runs
+    if (writer) C->need_pool = need;
+  } else if (!G.pending) {
     nv.status = 1;  // 2°: no live edge
   } else if (s.budget > 0 && (long long)v.c >= s.budget) {
     nv.status = 4;
   } else {
-    unsigned k = 1;
-    if (!s.unit)
-      while (k < (unsigned)WHEEL && __ldcg(s.bnev + ((b + k) & (WHEEL - 1))) == 0) ++k;
+    const unsigned k = (unsigned)(-G.negk);
     nv.delta = k;
     nv.t = v.t + k;
     nv.c = v.c + 1;
@@ -264,19 +305,6 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
     unsigned r = 128;
     while (r < per && r < 4096u) r <<= 1;
     nv.region = r;
-    // ring check: during this cycle's treat every event allocated by a cycle c' with
-    // t(c') + f1max > t was still live; the treat's allocations must not have reached it
-    const unsigned long long head = __ldcg(&C->ev_head);
-    unsigned long long oldest = head;
-    for (unsigned back = 0; back < (unsigned)WHEEL && back <= v.c; ++back) {
-      const unsigned slot = (v.c - back) & (WHEEL - 1);
-      if (__ldcg((const long long*)&C->hist_t[slot]) + s.f1max <= v.t) break;
-      oldest = __ldcg(&C->hist_head[slot]);
-    }
-    if (head - oldest > s.ev_mask + 1) {
-      nv.status = 8;  // live events may have been overwritten: the host grows the ring and re-runs
-      if (writer) C->need_pool = (long long)(head - oldest);
-    }
     if (writer) {
       if (npl + npp > C->peak_phantoms) C->peak_phantoms = npl + npp;
       C->acc[(v.c + 1) % 3].pend_lanes = npl;
@@ -285,6 +313,65 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
   }
   if (writer) C->view = nv;
   v = nv;
+}
+
+// ---------------------------------------------------------------------------
+// slab engine: the grid is cut into slabs along its last axis;
+// each slab keeps one ghost plane per neighbour.  Water arriving at a ghost
+// vertex is max-combined into ghost_out_* (stamp | cand | ~src | !via) and
+// handed to the owner, which applies it like a local arrival before its treat.
+// After the treat the owner's boundary labels refresh the neighbour's ghost
+// labels (stale by at most one cycle: they only weaken the Step-4 pruning,
+// which stays exact — SURVEY E6, E14).
+// ---------------------------------------------------------------------------
+__global__ void k_slab_propose(Dev s) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const View v = s.ctl->view;
+  if (v.status != ST_RUNNING) return;
+  long long need = 0;
+  s.ctl->prop = wheel_propose(s, v, &need);
+}
+
+// virtual slabs on one device: combine the proposals (element-wise max)
+__global__ void k_slab_reduce(Ctl* const* ctls, int nslabs) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (((volatile View*)&ctls[0]->view)->status != ST_RUNNING) return;
+  Prop g = ctls[0]->prop;
+  for (int i = 1; i < nslabs; ++i) {
+    const Prop p = ctls[i]->prop;
+    g.bhit = max(g.bhit, p.bhit); g.negk = max(g.negk, p.negk);
+    g.pending = max(g.pending, p.pending); g.overflow = max(g.overflow, p.overflow);
+  }
+  for (int i = 0; i < nslabs; ++i) ctls[i]->gprop = g;
+}
+
+// apply the water a neighbour handed over for this slab's boundary plane
+__global__ void __launch_bounds__(THREADS) k_slab_apply(Dev s, const unsigned long long* in, unsigned dst0) {
+  const View v = s.ctl->view;
+  if (v.status != ST_RUNNING || v.c == 0) return;
+  Acc* acc = &s.ctl->acc[v.c % 3];
+  for (unsigned i = blockIdx.x * THREADS + threadIdx.x; i < s.plane; i += gridDim.x * THREADS) {
+    const unsigned long long w = __ldcg(in + i);
+    if ((unsigned)(w >> 48) != v.stamp) continue;
+    const unsigned D = dst0 + i;
+    const int cand = (int)((w >> 32) & 0xFFFFu);
+    const unsigned src = 0x7FFFFFFFu - (unsigned)((w >> 1) & 0x7FFFFFFFu);
+    const unsigned via = (w & 1) ? 0u : 1u;
+    const unsigned old = atomicMax(tmp_ptr(s.sw, D), (v.stamp << 16) | (unsigned)cand);
+    arrive_post(s, v, acc, old, D, cand, src, via);
+  }
+}
+
+// boundary labels -> plane buffer, and plane buffer -> ghost labels
+__global__ void __launch_bounds__(THREADS) k_slab_gather_labels(Dev s, unsigned src0, unsigned* out) {
+  for (unsigned i = blockIdx.x * THREADS + threadIdx.x; i < s.plane; i += gridDim.x * THREADS)
+    out[i] = *lbl_ptr(s.sw, src0 + i) & 0xFFFFu;
+}
+__global__ void __launch_bounds__(THREADS) k_slab_scatter_labels(Dev s, const unsigned* in, unsigned dst0) {
+  for (unsigned i = blockIdx.x * THREADS + threadIdx.x; i < s.plane; i += gridDim.x * THREADS) {
+    unsigned* lp = lbl_ptr(s.sw, dst0 + i);
+    if ((*lp & 0xFFFFu) != LBL_REMOVED) *lp = in[i];
+  }
 }
 
 // Maintenance (rare): forget stale temps and refresh lane-expiry times so the

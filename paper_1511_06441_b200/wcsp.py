@@ -47,7 +47,7 @@ class _Options(ctypes.Structure):
     _fields_ = [("time_mode", ctypes.c_int32), ("engine", ctypes.c_int32), ("demote_twin", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("cycle_budget", ctypes.c_int64),
                 ("phantom_capacity", ctypes.c_int64), ("trace_cap", ctypes.c_int64),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("slabs", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 class _Result(ctypes.Structure):
@@ -185,7 +185,8 @@ class Solver:
 
     def __init__(self, inst=None, *, shape=None, f1=None, f2=None, maskA=None, maskB=None, present=None,
                  M=None, time_mode: str = "jump", engine: str = "persistent", trace_cap: int = 0,
-                 phantom_capacity: int = 0, cycle_budget: int = 0, device: int = 0, stream=None):
+                 phantom_capacity: int = 0, cycle_budget: int = 0, device: int = 0, stream=None,
+                 slabs: int = 0):
         lib = load_library()
         self._lib = lib
         self._h = ctypes.c_void_p()
@@ -203,6 +204,7 @@ class Solver:
         o.phantom_capacity = int(phantom_capacity)
         o.trace_cap = int(trace_cap)
         o.stream = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        o.slabs = int(slabs)
         self.trace_cap = int(trace_cap)
         p, keep = _problem(self.shape, f1, f2, maskA, maskB, present, M)
         st = lib.wcsp_create(ctypes.byref(p), ctypes.byref(o), ctypes.byref(self._h))

@@ -266,3 +266,35 @@ def test_fractal_C4(engine):
         want = (wcsp.REACHED, t, t, f.index((t, t)), f.index((t, t - 1)))
         r2 = wcsp.solve(f.with_M(t + 1), engine=engine)
         assert r2.key() == want
+
+
+@pytest.mark.parametrize("slabs", [2, 3, 5])
+def test_slab_engine(slabs):
+    """the grid cut into slabs along its last axis (ghost planes,
+    one exchange of boundary water and labels per cycle, max-combined cycle
+    decisions) gives exactly the single-device outputs (reading R24); stale
+    ghost labels may only add work."""
+    rng = np.random.default_rng(700 + slabs)
+    shapes = [(12, 12), (9, 20), (6, 6, 6), (5, 4, 11), (3, 3, 3, 8), (40,)]
+    for i in range(60):
+        inst = I.random_small(rng, shapes=shapes, M_range=(5, 120), max_sources=4, max_targets=4,
+                              hole_prob=0.1 if i % 3 == 0 else 0.0)
+        if i % 7 == 3:
+            inst = inst.with_M(I.M_INF)
+        if i % 5 == 4:
+            inst = inst.with_sets(present=(rng.random(inst.N) > 0.1).astype(np.uint8))
+            if not (inst.maskA & inst.present).any() or not (inst.maskB & inst.present).any():
+                continue
+        if inst.shape[-1] < slabs:
+            continue
+        o = oracle.solve_pruned(inst)
+        r = wcsp.solve(inst, engine="wheel", slabs=slabs)
+        assert r.key() == o.key(), (inst.shape, inst.M, slabs, r, o)
+        assert r.edge_updates >= o.work
+    for inst in (I.config_face((64, 64), 1, 300), I.config_face((32, 32, 32), 2, 200), I.fixture_D()):
+        if inst.shape[-1] < slabs:
+            continue
+        r1 = wcsp.solve(inst, engine="wheel")
+        rs = wcsp.solve(inst, engine="wheel", slabs=slabs)
+        assert rs.key() == r1.key() == oracle.solve_pruned(inst).key()
+        assert rs.edge_updates >= r1.edge_updates

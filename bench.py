@@ -62,6 +62,27 @@ def workload_instance(name: str, seed: int):
     return I.config_face(WORKLOADS[name]["shape"], seed, M, name=name), table[key]
 
 
+def share_nccl_id(rank: int) -> bytes:
+    """NCCL unique id of the multi-GPU slab engine: made on rank 0, shared
+    through torch.distributed (any backend)."""
+    import torch.distributed as dist
+    from paper_1511_06441_b200 import wcsp
+    obj = [wcsp.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def reduce_timing(total_ms: float, units: float, device: str):
+    """(max over ranks of the device time, sum over ranks of the work)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+    u = torch.tensor([float(units)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
 def alg_bytes(r, d: int, engine: str) -> int:
     """Algorithmic bytes per solve.
     sweep engines (SURVEY §8(d) 'alg'): 2 B per live lane/phantom per cycle
@@ -184,6 +205,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--partition", default="replicas", choices=["replicas", "slabs"],
+                    help="N > 1: independent seeds per rank (weak) or one instance cut into z-slabs (strong)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -196,10 +219,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1511_06441_b200 import wcsp
 
-    inst, meta = workload_instance(args.workload, rank)
+    slabs = world > 1 and args.partition == "slabs"
+    inst, meta = workload_instance(args.workload, 0 if slabs else rank)
     d = len(inst.shape)
     stream = torch.cuda.current_stream()
-    solver = wcsp.Solver(inst, engine=args.engine, stream=stream)
+    if slabs:   # one instance, slab `rank` of `world` on this GPU, NCCL exchange every cycle
+        solver = wcsp.Solver(inst, engine="wheel", stream=stream, nranks=world, rank=rank,
+                             nccl_id=share_nccl_id(rank))
+    else:
+        solver = wcsp.Solver(inst, engine=args.engine, stream=stream)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > L2 (126 MB)
 
     for _ in range(args.warmup):
@@ -225,11 +253,8 @@ def main():
     total_ms = sum(step_ms)
     updates = sum(r.edge_updates for r in results)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        u = torch.tensor([updates], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(u, op=torch.distributed.ReduceOp.SUM)
-        total_ms, updates_all = float(t.item()), float(u.item())
+        # slabs: every rank reports the whole instance's (summed) work; count it once
+        total_ms, updates_all = reduce_timing(total_ms, updates / world if slabs else updates, "cuda")
     else:
         updates_all = updates
     value = updates_all / (total_ms / 1000.0)
@@ -257,7 +282,7 @@ def main():
 
     # e2e through the C-ABI with host buffers (pinned): H2D of the step's inputs + solve + result read
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not slabs:
         pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(inst, k))).pin_memory()
                for k in ("f1", "f2", "maskA", "maskB")}
         host = {k: v.numpy() for k, v in pin.items()}
@@ -276,12 +301,7 @@ def main():
             e_upd += rr.edge_updates
         et = sum(e_ms)
         if world > 1:
-            t = torch.tensor([et], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            et = float(t.item())
-            u = torch.tensor([e_upd], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(u, op=torch.distributed.ReduceOp.SUM)
-            e_upd = float(u.item())
+            et, e_upd = reduce_timing(et, e_upd / world if slabs else e_upd, "cuda")
         e2e = {"value": e_upd / (et / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 312, "ms_per_step": et / args.e2e_steps,
                "path": "wcsp_load (pinned host f1,f2,A,B -> HBM, validate, weight build) + wcsp_solve + result D2H"}
@@ -297,12 +317,14 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+            "scaling": "strong" if slabs else "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
                        "shape": list(inst.shape), "seed": meta["seed"], "M": inst.M,
                        "M_bind_from": "paper_1511_06441_b200/data/mbind.json (oracle, scripts/make_mbind.py)",
                        "engine": args.engine, "l2": "flushed between steps (256 MiB write outside the events)",
-                       "parallelism": f"{world} independent instances (one seed per rank)" if world > 1 else "1 GPU"},
+                       "parallelism": (f"{world} z-slabs of one instance (NCCL send/recv + allreduce per cycle)"
+                                       if slabs else f"{world} independent instances (one seed per rank)")
+                                      if world > 1 else "1 GPU"},
             "solve_ms": total_ms / args.steps,
             "solve": {"F1": r0.F1, "F2": r0.F2, "X": r0.X, "Y": r0.Y, "cycles": r0.cycles,
                       "edge_updates": r0.edge_updates, "arrivals": r0.arrivals, "triggered": r0.triggered,

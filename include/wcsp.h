@@ -102,6 +102,14 @@ typedef struct {
                                a slab boundary every cycle (the multi-GPU layout run
                                on one GPU); requires engine WHEEL and host arrays.  0/1 = off. */
   int32_t reserved0;
+  int32_t nranks;           /* > 1: multi-GPU slab engine — this process owns slab `rank` of `nranks`
+                               (one process per GPU); the slabs exchange boundary water and labels
+                               with ncclSend/ncclRecv and combine the cycle decision with one
+                               ncclAllReduce(max) per cycle.  Every rank passes the whole problem
+                               (host arrays) and the same nccl_id. */
+  int32_t rank;
+  const uint8_t* nccl_id;   /* 128 bytes from wcsp_nccl_unique_id() on one rank, shared with all;
+                               non-NULL with nranks = 1 runs the NCCL path on one GPU */
 } wcsp_options;
 
 typedef struct {
@@ -168,6 +176,9 @@ wcsp_status wcsp_trace(wcsp_handle* h, wcsp_trace_rec* out, int64_t cap, int64_t
  * WCSP_EINVAL otherwise.  Host arrays only. */
 wcsp_status wcsp_validate_path(const wcsp_problem* problem, const int64_t* path, int64_t len,
                                int64_t* F1, int64_t* F2);
+/* NCCL unique id (128 bytes) for options.nccl_id; call on one rank and share it
+ * (e.g. through torch.distributed).  Returns WCSP_ENCCL if NCCL cannot be loaded. */
+wcsp_status wcsp_nccl_unique_id(uint8_t* out128);
 void wcsp_destroy(wcsp_handle* h);
 const char* wcsp_last_error(void);
 /* Version string, and the number of SMs / cooperative blocks the persistent engine uses. */

@@ -5,6 +5,8 @@
 #include "wcsp_wheel.cuh"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -91,6 +93,8 @@ struct wcsp_handle {
   unsigned long long preset_nB = 0;                  // child: |B| of the whole problem (B-arrival list)
   std::vector<wcsp_handle*> children;                // parent of a virtual slab group
   Ctl** d_ctls = nullptr;                            // children's control blocks (device array)
+  void* comm = nullptr;                              // ncclComm_t (multi-GPU slab engine)
+  int rank = 0, nranks = 1;
 };
 
 namespace {
@@ -299,7 +303,11 @@ wcsp_status load_problem(wcsp_handle* h, const wcsp_problem* p) {
   return WCSP_REACHED;
 }
 
+void destroy_comm(void* comm);
+
 void release(wcsp_handle* h) {
+  if (h->comm) destroy_comm(h->comm);
+  h->comm = nullptr;
   for (wcsp_handle* c : h->children) {
     release(c);
     delete c;
@@ -617,6 +625,42 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
 // device-to-device copies and k_slab_reduce by NCCL send/recv and an
 // allreduce(max); the kernels are the same.
 // ---------------------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  const char* path = getenv("WCSP_NCCL_LIB");
+  void* lib = dlopen(path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) return api;
+  api.getUniqueId = (decltype(api.getUniqueId))dlsym(lib, "ncclGetUniqueId");
+  api.commInitRank = (decltype(api.commInitRank))dlsym(lib, "ncclCommInitRank");
+  api.commDestroy = (decltype(api.commDestroy))dlsym(lib, "ncclCommDestroy");
+  api.send = (decltype(api.send))dlsym(lib, "ncclSend");
+  api.recv = (decltype(api.recv))dlsym(lib, "ncclRecv");
+  api.allReduce = (decltype(api.allReduce))dlsym(lib, "ncclAllReduce");
+  api.groupStart = (decltype(api.groupStart))dlsym(lib, "ncclGroupStart");
+  api.groupEnd = (decltype(api.groupEnd))dlsym(lib, "ncclGroupEnd");
+  api.errStr = (decltype(api.errStr))dlsym(lib, "ncclGetErrorString");
+  api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.send && api.recv && api.allReduce &&
+           api.groupStart && api.groupEnd && api.errStr;
+  return api;
+}
+
 wcsp_status host_validate(const wcsp_problem* p, unsigned long long* nB, int* f1max) {
   long long N = 1, st[4] = {1, 1, 1, 1};
   for (int k = 0; k < p->d; ++k) { st[k] = N; N *= p->shape[k]; }
@@ -646,7 +690,11 @@ wcsp_status host_validate(const wcsp_problem* p, unsigned long long* nB, int* f1
 wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_handle** out) {
   if (p->mem != WCSP_MEM_HOST) return fail(WCSP_EINVAL, "the slab engine takes host arrays");
   if (!is_wheel(opt.engine)) return fail(WCSP_EINVAL, "the slab engine runs the wheel engine (engine = WHEEL)");
-  const int R = opt.slabs, d = p->d;
+  const bool dist = opt.nccl_id != nullptr && opt.nranks >= 1;   // nranks = 1: NCCL path on one GPU (tests)
+  if (dist && (opt.rank < 0 || opt.rank >= opt.nranks || !opt.nccl_id))
+    return fail(WCSP_EINVAL, "multi-GPU slab engine needs 0 <= rank < nranks and nccl_id");
+  if (dist && !nccl_api().ok) return fail(WCSP_ENCCL, "cannot load libnccl.so.2 (set WCSP_NCCL_LIB)");
+  const int R = dist ? opt.nranks : opt.slabs, d = p->d;
   const long long nL = p->shape[d - 1];
   if (nL < R) return fail(WCSP_EINVAL, "last axis (%lld) shorter than the number of slabs (%d)", nL, R);
   long long N = 1;
@@ -676,7 +724,10 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
   if (cudaEventCreate(&g->e0) != cudaSuccess || cudaEventCreate(&g->e1) != cudaSuccess ||
       cudaEventCreate(&g->em) != cudaSuccess)
     return bail(fail(WCSP_ECUDA, "event creation failed"));
+  g->rank = dist ? opt.rank : 0;
+  g->nranks = dist ? opt.nranks : 1;
   for (int i = 0; i < R; ++i) {
+    if (dist && i != opt.rank) continue;          // one slab per process
     SlabSpec sp{};
     sp.index = i;
     sp.z0 = (long long)i * nL / R;
@@ -718,6 +769,14 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
     wcsp_handle* ch = nullptr;
     if ((st = create_impl(&lp, co, &sp, &ch)) != WCSP_REACHED) return bail(st);
     g->children.push_back(ch);
+  }
+  if (dist) {
+    ncclUniqueId id;
+    memcpy(&id, opt.nccl_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    const ncclResult_t nr = nccl_api().commInitRank(&comm, opt.nranks, id, opt.rank);
+    if (nr != ncclSuccess) return bail(fail(WCSP_ENCCL, "ncclCommInitRank: %s", nccl_api().errStr(nr)));
+    g->comm = comm;
   }
   std::vector<Ctl*> ctls;
   for (auto* ch : g->children) ctls.push_back(ch->ctl);
@@ -850,11 +909,148 @@ wcsp_status group_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
   return WCSP_REACHED;
 }
 
+// ---------------------------------------------------------------------------
+// NCCL transport of the slab engine (one process per GPU).  NCCL is loaded
+// with dlopen on first use (the process normally already holds torch's
+// libnccl.so.2), so the library itself does not depend on it.
+// ---------------------------------------------------------------------------
+void destroy_comm(void* comm) {
+  if (comm && nccl_api().ok) nccl_api().commDestroy((ncclComm_t)comm);
+}
+
+#define NCK(call)                                                                                       \
+  do {                                                                                                  \
+    ncclResult_t r_ = (call);                                                                           \
+    if (r_ != ncclSuccess) return fail(WCSP_ENCCL, "%s: %s (%s:%d)", #call, nccl_api().errStr(r_), __FILE__, \
+                                       __LINE__);                                                       \
+  } while (0)
+
+// One cycle of the distributed slab engine (this rank's slab = children[0]).
+template <int D>
+wcsp_status dist_cycle(wcsp_handle* g, const Dev& dv) {
+  NcclApi& nc = nccl_api();
+  wcsp_handle* c = g->children[0];
+  const size_t sm = sizeof(Smem), pl = g->plane;
+  const int pg = (int)std::min<unsigned long long>((pl + THREADS - 1) / THREADS, (unsigned long long)g->grid);
+  cudaStream_t s = g->stream;
+  ncclComm_t comm = (ncclComm_t)g->comm;
+  const int lo = g->rank - 1, hi = g->rank + 1;
+  k_wheel_fire<D><<<c->grid, THREADS, sm, s>>>(dv);
+  NCK(nc.groupStart());             // water that crossed a slab boundary goes to its owner
+  if (c->glo) { NCK(nc.send(c->g_out_lo, pl, ncclUint64, lo, comm, s)); NCK(nc.recv(c->g_in_lo, pl, ncclUint64, lo, comm, s)); }
+  if (c->ghi) { NCK(nc.send(c->g_out_hi, pl, ncclUint64, hi, comm, s)); NCK(nc.recv(c->g_in_hi, pl, ncclUint64, hi, comm, s)); }
+  NCK(nc.groupEnd());
+  if (c->glo) k_slab_apply<<<pg, THREADS, 0, s>>>(dv, c->g_in_lo, c->plane);
+  if (c->ghi) k_slab_apply<<<pg, THREADS, 0, s>>>(dv, c->g_in_hi, c->ghost_hi_start - c->plane);
+  k_wheel_treat<D><<<c->grid, THREADS, sm, s>>>(dv);
+  if (c->glo) k_slab_gather_labels<<<pg, THREADS, 0, s>>>(dv, c->plane, c->l_out_lo);
+  if (c->ghi) k_slab_gather_labels<<<pg, THREADS, 0, s>>>(dv, c->ghost_hi_start - c->plane, c->l_out_hi);
+  NCK(nc.groupStart());             // boundary labels refresh the neighbours' ghost planes
+  if (c->glo) { NCK(nc.send(c->l_out_lo, pl, ncclUint32, lo, comm, s)); NCK(nc.recv(c->l_in_lo, pl, ncclUint32, lo, comm, s)); }
+  if (c->ghi) { NCK(nc.send(c->l_out_hi, pl, ncclUint32, hi, comm, s)); NCK(nc.recv(c->l_in_hi, pl, ncclUint32, hi, comm, s)); }
+  NCK(nc.groupEnd());
+  if (c->glo) k_slab_scatter_labels<<<pg, THREADS, 0, s>>>(dv, c->l_in_lo, 0u);
+  if (c->ghi) k_slab_scatter_labels<<<pg, THREADS, 0, s>>>(dv, c->l_in_hi, c->ghost_hi_start);
+  k_slab_propose<<<1, 32, 0, s>>>(dv);
+  NCK(nc.allReduce(&c->ctl->prop, &c->ctl->gprop, 4, ncclInt64, ncclMax, comm, s));
+  k_wheel_decide<<<1, 32, 0, s>>>(dv);
+  g->launches += 5 + (c->glo + c->ghi) * 3;
+  return WCSP_REACHED;
+}
+
+wcsp_status dist_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
+  wcsp_status st;
+  NcclApi& nc = nccl_api();
+  wcsp_handle* c = g->children[0];
+  ncclComm_t comm = (ncclComm_t)g->comm;
+  g->launches = 0;
+  CK(cudaEventRecord(g->e0, g->stream));
+  c->M = g->M;
+  if ((st = reset_ctl(c)) != WCSP_REACHED) return st;
+  if ((st = launch_init(c)) != WCSP_REACHED) return st;
+  g->launches += 1;
+  CK(cudaEventRecord(g->em, g->stream));
+  const Dev dv = make_dev(c);
+  int batch = 4;
+  for (;;) {
+    for (int i = 0; i < batch; ++i) {
+      switch (g->d) {
+        case 1: st = dist_cycle<1>(g, dv); break;
+        case 2: st = dist_cycle<2>(g, dv); break;
+        case 3: st = dist_cycle<3>(g, dv); break;
+        default: st = dist_cycle<4>(g, dv); break;
+      }
+      if (st != WCSP_REACHED) return st;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&g->h_ctl->view, &c->ctl->view, sizeof(View), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    const int s0 = g->h_ctl->view.status;   // identical on every rank (decisions use the reduced proposal)
+    if (s0 == ST_WRAP) {
+      k_wheel_maintain<<<c->grid, THREADS, 0, g->stream>>>(dv);
+      const int run = ST_RUNNING;
+      CK(cudaMemcpyAsync(&c->ctl->view.status, &run, sizeof(int), cudaMemcpyHostToDevice, g->stream));
+      CK(cudaStreamSynchronize(g->stream));
+      continue;
+    }
+    if (s0 != ST_RUNNING) break;
+    batch = std::min(batch * 2, 64);
+  }
+  CK(cudaEventRecord(g->e1, g->stream));
+  // totals over the ranks: counters (sum), Y (min), overflow need (max)
+  Ctl cs;
+  CK(cudaMemcpyAsync(&cs, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  long long sums[8] = {cs.edge_updates, cs.arrivals, cs.triggered, cs.created, cs.relabels, cs.started,
+                       cs.peak_phantoms, 0};
+  unsigned long long mins[2] = {cs.ybest, 0}, maxs[2] = {(unsigned long long)std::max(0ll, cs.need_pool),
+                                                         cs.need_pool == -2 ? 1ull : 0ull};
+  long long* dsum = nullptr;
+  unsigned long long *dmin = nullptr, *dmax = nullptr;
+  CK(cudaMalloc(&dsum, sizeof(sums)));
+  CK(cudaMalloc(&dmin, sizeof(mins)));
+  CK(cudaMalloc(&dmax, sizeof(maxs)));
+  CK(cudaMemcpyAsync(dsum, sums, sizeof(sums), cudaMemcpyHostToDevice, g->stream));
+  CK(cudaMemcpyAsync(dmin, mins, sizeof(mins), cudaMemcpyHostToDevice, g->stream));
+  CK(cudaMemcpyAsync(dmax, maxs, sizeof(maxs), cudaMemcpyHostToDevice, g->stream));
+  NCK(nc.allReduce(dsum, dsum, 8, ncclInt64, ncclSum, comm, g->stream));
+  NCK(nc.allReduce(dmin, dmin, 2, ncclUint64, ncclMin, comm, g->stream));
+  NCK(nc.allReduce(dmax, dmax, 2, ncclUint64, ncclMax, comm, g->stream));
+  CK(cudaMemcpyAsync(sums, dsum, sizeof(sums), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaMemcpyAsync(mins, dmin, sizeof(mins), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaMemcpyAsync(maxs, dmax, sizeof(maxs), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  cudaFree(dsum); cudaFree(dmin); cudaFree(dmax);
+  float ms = 0, cms = 0;
+  CK(cudaEventElapsedTime(&ms, g->e0, g->e1));
+  CK(cudaEventElapsedTime(&cms, g->em, g->e1));
+  *status = cs.view.status;
+  memset(r, 0, sizeof(*r));
+  r->edge_updates = sums[0]; r->arrivals = sums[1]; r->triggered = sums[2]; r->phantoms_created = sums[3];
+  r->relabels = sums[4]; r->lanes_started = sums[5]; r->peak_phantoms = sums[6];
+  r->cycles = cs.cycles;
+  c->last_cycles = g->last_cycles = cs.cycles;
+  if (*status == WCSP_REACHED) {
+    r->F1 = cs.F1; r->F2 = cs.F2; r->X = cs.X;
+    r->Y = mins[0] == ~0ull ? -1 : (long long)(mins[0] >> 1);
+    r->via_phantom = (int)(mins[0] & 1);
+    r->x_lane = x_lane_of(g, r->X, r->Y);
+  } else {
+    r->F1 = r->F2 = r->X = r->Y = -1;
+    r->x_lane = -1;
+  }
+  r->phantom_capacity = *status == WCSP_EOVERFLOW ? (maxs[1] ? -2 : (long long)maxs[0]) : (long long)c->ev_cap;
+  r->kernel_launches = g->launches;
+  r->device_ms = ms;
+  r->cycle_ms = cms;
+  return WCSP_REACHED;
+}
+
 wcsp_status group_solve(wcsp_handle* g, wcsp_result* out) {
   wcsp_result r;
   int status = ST_RUNNING;
   for (int attempt = 0; attempt < 6; ++attempt) {
-    wcsp_status st = group_solve_once(g, &r, &status);
+    wcsp_status st = g->comm ? dist_solve_once(g, &r, &status) : group_solve_once(g, &r, &status);
     if (st != WCSP_REACHED) return st;
     if (status != WCSP_EOVERFLOW) break;
     for (auto* c : g->children) {     // grow every child's wheel storage and re-run
@@ -897,7 +1093,7 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
     return fail(WCSP_EINVAL, "bad engine %d", opt.engine);
   if (opt.trace_cap < 0 || opt.cycle_budget < 0 || opt.phantom_capacity < 0) return fail(WCSP_EINVAL, "negative option");
 
-  if (opt.slabs > 1) return create_group(p, opt, out);
+  if (opt.slabs > 1 || opt.nranks > 1 || opt.nccl_id) return create_group(p, opt, out);
   return create_impl(p, opt, nullptr, out);
 }
 
@@ -1068,6 +1264,16 @@ wcsp_status wcsp_validate_path(const wcsp_problem* p, const int64_t* path, int64
   *F1 = s1;
   *F2 = s2;
   if (p->M != WCSP_M_INF && s2 >= p->M) return WCSP_INFEASIBLE;
+  return WCSP_REACHED;
+}
+
+wcsp_status wcsp_nccl_unique_id(uint8_t* out128) {
+  if (!out128) return fail(WCSP_EINVAL, "NULL argument");
+  if (!nccl_api().ok) return fail(WCSP_ENCCL, "cannot load libnccl.so.2 (set WCSP_NCCL_LIB)");
+  ncclUniqueId id;
+  const ncclResult_t r = nccl_api().getUniqueId(&id);
+  if (r != ncclSuccess) return fail(WCSP_ENCCL, "ncclGetUniqueId: %s", nccl_api().errStr(r));
+  memcpy(out128, &id, sizeof(id));
   return WCSP_REACHED;
 }
 

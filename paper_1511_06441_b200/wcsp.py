@@ -47,7 +47,8 @@ class _Options(ctypes.Structure):
     _fields_ = [("time_mode", ctypes.c_int32), ("engine", ctypes.c_int32), ("demote_twin", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("cycle_budget", ctypes.c_int64),
                 ("phantom_capacity", ctypes.c_int64), ("trace_cap", ctypes.c_int64),
-                ("stream", ctypes.c_void_p), ("slabs", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("stream", ctypes.c_void_p), ("slabs", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
 
 
 class _Result(ctypes.Structure):
@@ -70,7 +71,7 @@ class _TraceRec(ctypes.Structure):
 
 
 EXPORTS = ["wcsp_create", "wcsp_load", "wcsp_solve", "wcsp_set_targets", "wcsp_reconstruct", "wcsp_trace",
-           "wcsp_validate_path", "wcsp_destroy", "wcsp_last_error", "wcsp_version"]
+           "wcsp_validate_path", "wcsp_destroy", "wcsp_last_error", "wcsp_version", "wcsp_nccl_unique_id"]
 
 _lib = None
 
@@ -103,6 +104,8 @@ def load_library(path: str = LIB_PATH):
     lib.wcsp_destroy.restype = None
     lib.wcsp_last_error.restype = ctypes.c_char_p
     lib.wcsp_version.restype = ctypes.c_char_p
+    lib.wcsp_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    lib.wcsp_nccl_unique_id.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -186,7 +189,7 @@ class Solver:
     def __init__(self, inst=None, *, shape=None, f1=None, f2=None, maskA=None, maskB=None, present=None,
                  M=None, time_mode: str = "jump", engine: str = "persistent", trace_cap: int = 0,
                  phantom_capacity: int = 0, cycle_budget: int = 0, device: int = 0, stream=None,
-                 slabs: int = 0):
+                 slabs: int = 0, nranks: int = 1, rank: int = 0, nccl_id: bytes = None):
         lib = load_library()
         self._lib = lib
         self._h = ctypes.c_void_p()
@@ -205,6 +208,13 @@ class Solver:
         o.trace_cap = int(trace_cap)
         o.stream = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         o.slabs = int(slabs)
+        o.nranks = int(nranks)
+        o.rank = int(rank)
+        self._nccl_id = None
+        if nccl_id is not None:
+            assert len(nccl_id) == 128
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         self.trace_cap = int(trace_cap)
         p, keep = _problem(self.shape, f1, f2, maskA, maskB, present, M)
         st = lib.wcsp_create(ctypes.byref(p), ctypes.byref(o), ctypes.byref(self._h))
@@ -289,6 +299,15 @@ def validate_path(inst, path):
     f1, f2 = ctypes.c_int64(0), ctypes.c_int64(0)
     st = lib.wcsp_validate_path(ctypes.byref(p), arr, len(path), ctypes.byref(f1), ctypes.byref(f2))
     return int(st), int(f1.value), int(f2.value)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for Solver(nranks > 1, nccl_id=...); share it from one rank."""
+    buf = ctypes.create_string_buffer(128)
+    st = load_library().wcsp_nccl_unique_id(buf)
+    if st != REACHED:
+        raise WcspError(st, last_error())
+    return buf.raw
 
 
 def version() -> str:

@@ -298,3 +298,16 @@ def test_slab_engine(slabs):
         rs = wcsp.solve(inst, engine="wheel", slabs=slabs)
         assert rs.key() == r1.key() == oracle.solve_pruned(inst).key()
         assert rs.edge_updates >= r1.edge_updates
+
+
+def test_slab_engine_nccl_single_rank():
+    """The multi-GPU transport (NCCL send/recv + allreduce per cycle) on one
+    rank: the allreduce path and the distributed driver give the single-device
+    outputs and counters."""
+    for inst in (I.config_face((48, 48), 3, 220), I.config_face((16, 16, 16), 1, 120), I.fixture_B(),
+                 I.speedway_instance(12)):
+        r1 = wcsp.solve(inst, engine="wheel")
+        with wcsp.Solver(inst, engine="wheel", nranks=1, rank=0, nccl_id=wcsp.nccl_unique_id()) as s:
+            rn = s.solve()
+        assert rn.key() == r1.key()
+        assert (rn.edge_updates, rn.cycles, rn.phantoms_created) == (r1.edge_updates, r1.cycles, r1.phantoms_created)

@@ -173,7 +173,8 @@ def run_reference(args, rank, world):
     inst, meta = workload_instance(args.workload, 0)
     import oracle
     oracle.build()
-    r, dt, t_limit = cpu_sample(inst, target_s=args.ref_seconds)
+    # each step a bounded sample sized so the whole W + K run stays within ~2.5 minutes
+    r, dt, t_limit = cpu_sample(inst, target_s=min(args.ref_seconds, 150.0 / max(1, args.warmup + args.steps)))
     times, work = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()

@@ -148,6 +148,8 @@ typedef struct {
   int64_t tested;           /* triggered-bitmap entries examined by the treat phase */
   int64_t ns_arrive;        /* device ns of the arrival phase (sweep / fire) incl. its grid barrier */
   int64_t ns_treat;         /* device ns of the treat phase incl. its grid barrier */
+  int64_t ns_arrive_spread; /* wheel persistent: last minus first block to finish the arrival phase */
+  int64_t ns_treat_spread;  /* ... the treat phase (load imbalance) */
 } wcsp_trace_rec;
 
 typedef struct wcsp_handle wcsp_handle;
@@ -176,6 +178,16 @@ wcsp_status wcsp_trace(wcsp_handle* h, wcsp_trace_rec* out, int64_t cap, int64_t
  * WCSP_EINVAL otherwise.  Host arrays only. */
 wcsp_status wcsp_validate_path(const wcsp_problem* problem, const int64_t* path, int64_t len,
                                int64_t* F1, int64_t* F2);
+/* The whole F1*(M) staircase in one run (PAPER.md:21 for every
+ * budget at once): run with M = M_max past the first arrival at B and record every
+ * arrival that beats all earlier ones — step i = (F1_i, F2_i, X_i, Y_i), F1 increasing,
+ * F2 decreasing.  The constrained optimum for any budget M <= M_max is the first step
+ * with F2_i < M (infeasible if none).  The run ends when nothing is live or a step
+ * reaches F2 <= f2_stop.  steps: caller-allocated [cap][4]; *n = number of steps (may
+ * exceed cap).  Wheel engine, single device.  Returns WCSP_REACHED if a step exists,
+ * else WCSP_INFEASIBLE; result = the last step's solve record. */
+wcsp_status wcsp_staircase(wcsp_handle* h, int64_t M_max, int64_t f2_stop, int64_t* steps, int64_t cap,
+                           int64_t* n, wcsp_result* result);
 /* NCCL unique id (128 bytes) for options.nccl_id; call on one rank and share it
  * (e.g. through torch.distributed).  Returns WCSP_ENCCL if NCCL cannot be loaded. */
 wcsp_status wcsp_nccl_unique_id(uint8_t* out128);

@@ -31,10 +31,12 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= max(os.path.getmtime(p) for p in DEPS):
-        return SO
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", SO + ".tmp", *SOURCES, "-ldl"]
+def build(force: bool = False, verbose: bool = False, out: str = SO, defines=()) -> str:
+    """Compile libwcsp.so (or a variant `out` with extra -D `defines`, for A/B runs)."""
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(p) for p in DEPS):
+        return out
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o",
+           out + ".tmp", *SOURCES, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
     with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
@@ -44,9 +46,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libwcsp.so")
     if verbose:
         sys.stdout.write(log)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    build(force="--force" in sys.argv or bool(defs), verbose=True, out=outs[0] if outs else SO, defines=defs)

@@ -95,6 +95,10 @@ struct wcsp_handle {
   Ctl** d_ctls = nullptr;                            // children's control blocks (device array)
   void* comm = nullptr;                              // ncclComm_t (multi-GPU slab engine)
   int rank = 0, nranks = 1;
+  int staircase = 0;                                 // wcsp_staircase in progress
+  long long f2stop = 0;
+  long long* stair = nullptr;
+  unsigned stair_cap = 0;
 };
 
 namespace {
@@ -173,6 +177,10 @@ Dev make_dev(const wcsp_handle* h) {
   s.ghost_out_lo = h->g_out_lo;
   s.ghost_out_hi = h->g_out_hi;
   s.slab = h->slab_index >= 0;
+  s.staircase = h->staircase;
+  s.f2stop = h->f2stop;
+  s.stair = h->stair;
+  s.stair_cap = h->stair_cap;
   return s;
 }
 
@@ -316,7 +324,7 @@ void release(wcsp_handle* h) {
   void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->tbits, h->barr,
                   h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
                   h->d_cnt, h->d_ghost, h->g_out_lo, h->g_out_hi, h->g_in_lo, h->g_in_hi, h->l_out_lo,
-                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls};
+                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -1265,6 +1273,41 @@ wcsp_status wcsp_validate_path(const wcsp_problem* p, const int64_t* path, int64
   *F2 = s2;
   if (p->M != WCSP_M_INF && s2 >= p->M) return WCSP_INFEASIBLE;
   return WCSP_REACHED;
+}
+
+wcsp_status wcsp_staircase(wcsp_handle* h, int64_t M_max, int64_t f2_stop, int64_t* steps, int64_t cap,
+                           int64_t* n, wcsp_result* result) {
+  if (!h || !n || (cap > 0 && !steps)) return fail(WCSP_EINVAL, "NULL argument");
+  if (!h->children.empty() || !is_wheel(h->opt.engine))
+    return fail(WCSP_EINVAL, "wcsp_staircase needs a single-device wheel-engine handle");
+  wcsp_status st;
+  if ((st = check_M(M_max)) != WCSP_REACHED) return st;
+  CK(cudaSetDevice(h->dev));
+  const unsigned want = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, 1 << 24));
+  if (want > h->stair_cap) {
+    if (h->stair) cudaFree(h->stair);
+    h->stair = nullptr;
+    h->stair_cap = 0;
+    CK(cudaMalloc(&h->stair, (size_t)want * 4 * sizeof(long long)));
+    h->stair_cap = want;
+  }
+  const long long saved_M = h->M;
+  h->M = M_max;
+  h->staircase = 1;
+  h->f2stop = M_max == WCSP_M_INF ? (1ll << 62) : f2_stop;   // M = inf: every arrival has F2 = -1
+  wcsp_result r;
+  st = solve_impl(h, &r);
+  h->staircase = 0;
+  h->M = saved_M;
+  if (st != WCSP_REACHED && st != WCSP_INFEASIBLE) return st;
+  const long long k = h->h_ctl->n_stair;
+  *n = k;
+  const long long m = std::min<long long>(k, std::min<int64_t>(cap, h->stair_cap));
+  if (m > 0) {
+    CK(cudaMemcpy(steps, h->stair, (size_t)m * 4 * sizeof(long long), cudaMemcpyDeviceToHost));
+  }
+  if (result) *result = r;
+  return st;
 }
 
 wcsp_status wcsp_nccl_unique_id(uint8_t* out128) {

@@ -92,6 +92,7 @@ struct Ctl {
   long long cycles, edge_updates, arrivals, triggered, created, relabels, started;
   long long peak_active, peak_phantoms, need_pool;
   unsigned long long ts0, ts1, ts2;   // globaltimer at cycle start / after arrivals / after treat (block 0)
+  unsigned long long fin[2][2][2];    // [cycle & 1][phase][max, sum] block busy times (persistent engines)
   // timing-wheel engine (wcsp_wheel.cuh)
   unsigned long long ev_head;      // logical allocation head of the event ring
   unsigned wheel_overflow, pad2_;  // 2: descriptor table full
@@ -99,11 +100,14 @@ struct Ctl {
   unsigned long long hist_head[WHEEL];   // ... and the ring head before its treat
   Prop prop, gprop;                // slab engine: local proposal / reduced proposal
   unsigned long long ybest;        // (src << 1 | via) of the best arrival at X seen by this slab
+  unsigned n_stair, pad3_;         // staircase steps recorded
+  long long stair_q;               // best target quality so far
 };
 
 struct TraceRec {
   long long t, delta, active_vertices, live_lanes, phantoms, triggered, arrivals, created, relabels;
   long long tested, ns_arrive, ns_treat;   // bitmap entries examined; phase times seen by block 0
+  long long ns_arrive_spread, ns_treat_spread;   // max block busy time minus the mean (load imbalance)
 };
 
 struct Dev {
@@ -142,6 +146,11 @@ struct Dev {
   unsigned long long* ghost_out_lo;   // water handed to the lower neighbour's boundary plane
   unsigned long long* ghost_out_hi;   // ... to the upper neighbour's
   int slab;                        // 1: decide uses the reduced global proposal (ctl->gprop)
+  // staircase mode (wcsp_staircase): record every strictly better target arrival, keep going
+  int staircase;
+  long long f2stop;
+  long long* stair;                // [stair_cap][4] (F1, F2, X, Y)
+  unsigned stair_cap;
 };
 
 template <int D> struct Tr;
@@ -289,6 +298,7 @@ struct Smem {
   unsigned base_a, base_b, flag;
   View view;
   unsigned long long bhit;
+  unsigned long long tphase;       // globaltimer at the start of this block's phase
   unsigned long long red[WARPS][7];
   unsigned redmin[WARPS];
 };
@@ -569,7 +579,15 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
   return ((texp16 - (unsigned)t) & 0xFFFFu) - 1u < 255u;   // texp in (t, t + 255]
 }
 
-// Stage one event for the wheel (defined in wcsp_wheel.cuh).
+// Stage events for the wheel (defined in wcsp_wheel.cuh): at a reserved staging slot, or
+// one per predicated lane (warp-aggregated).
+#ifndef WCSP_TREAT_SCAN
+#define WCSP_TREAT_SCAN 0
+#endif
+#ifndef WCSP_FLUSH_MATCH
+#define WCSP_FLUSH_MATCH 0
+#endif
+__device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long long rec, unsigned delay, long long t);
 __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t);
 
 template <int D, bool WHEEL_ENGINE>
@@ -602,7 +620,7 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     swr[j] = test ? s.sw[q + s.off[j]] : 0xFFFFull;   // untested lanes read as "removed"
   }
   LW neww = 0;
-  unsigned fmax = 0;
+  unsigned fmax = 0, pm = 0;
 #pragma unroll
   for (int j = 0; j < 2 * D; ++j) {
     const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
@@ -617,10 +635,14 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     lanes_started += pass && inactive;                            // activate, time restored to f1 (:192)
     if constexpr (WHEEL_ENGINE) {
       if (pass && inactive) fmax = max(fmax, f1j);
+#if WCSP_TREAT_SCAN
+      if (pass) pm |= 1u << j;
+#else
       const unsigned long long rec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
                                      ((unsigned long long)(unsigned)c << PH_CAND) |
                                      ((unsigned long long)(inactive ? 1u : 0u) << 49);
       ev_push(s, sm, pass, rec, f1j, v.t);
+#endif
     } else {
       if (pass) dmin = min(dmin, f1j);
       if (pass && inactive) neww |= (LW)f1j << (8 * j);
@@ -630,6 +652,32 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       qpush<unsigned long long>(sm.qp, QP_CAP, &sm.np, ph, prec, &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
     }
   }
+#if WCSP_TREAT_SCAN
+  if constexpr (WHEEL_ENGINE) {     // one warp-level reservation for all of this Q's new edges
+    const unsigned lane = threadIdx.x & 31u, cnt = __popc(pm);
+    unsigned x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if ((int)lane >= o) x += y;
+    }
+    const unsigned total = __shfl_sync(0xFFFFFFFFu, x, 31);
+    unsigned base = 0;
+    if (lane == 31 && total) base = atomicAdd(&sm.np, total);
+    base = __shfl_sync(0xFFFFFFFFu, base, 31);
+    unsigned pos = base + x - cnt;
+    while (pm) {
+      const int j = __ffs(pm) - 1;
+      pm &= pm - 1u;
+      const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
+      const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
+      const unsigned long long rec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
+                                     ((unsigned long long)(unsigned)(lstar - (int)f2j) << PH_CAND) |
+                                     ((unsigned long long)(inactive ? 1u : 0u) << 49);
+      ev_stage(s, sm, pos++, rec, f1j, v.t);
+    }
+  }
+#endif
   if (inactive) {                                                 // Step 8.1
     relabels += 1;
     if constexpr (WHEEL_ENGINE) {
@@ -722,7 +770,7 @@ __device__ void decide(const Dev& s, View& v, bool writer) {
         const unsigned long long t2 = globaltimer_ns();
         TraceRec r{v.t, (long long)v.delta, (long long)v.n_act, (long long)live, (long long)v.n_pool,
                    (long long)triggered, (long long)arrivals, (long long)created, (long long)relabels,
-                   (long long)__ldcg(&a->tested), (long long)(C->ts1 - C->ts0), (long long)(t2 - C->ts1)};
+                   (long long)__ldcg(&a->tested), (long long)(C->ts1 - C->ts0), (long long)(t2 - C->ts1), 0, 0};
         s.trace[v.c - 1] = r;
       }
     }
@@ -768,9 +816,15 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // BARRIER_TIMEOUT_NS sets ctl->abort; every waiting block then gives up).
 constexpr unsigned long long BARRIER_TIMEOUT_NS = 20ull * 1000000000ull;
 
-__device__ __forceinline__ bool grid_sync(Ctl* ctl, unsigned long long target, Smem& sm) {
+__device__ __forceinline__ bool grid_sync(Ctl* ctl, unsigned long long target, Smem& sm,
+                                          unsigned long long* fin = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (fin) {                     // block busy time in this phase: max and sum over blocks
+      const unsigned long long busy = globaltimer_ns() - sm.tphase;
+      atomicMax(fin, busy);
+      atomicAdd(fin + 1, busy);
+    }
     __threadfence();
     atomicAdd(&ctl->bar, 1ull);
     const unsigned long long t0 = globaltimer_ns();

@@ -42,6 +42,19 @@ __device__ __forceinline__ void file_run(const Dev& s, unsigned b, unsigned long
   else atomicOr(&s.ctl->wheel_overflow, 2u);
 }
 
+__device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long long rec, unsigned delay, long long t) {
+  if (idx < (unsigned)QP_CAP) {
+    sm.qp[idx] = rec | ((unsigned long long)delay << EV_DELAY_SHIFT);
+  } else {                          // rare: staging full, file the event as a run of one
+    const unsigned long long pos = atomicAdd(&s.ctl->ev_head, 1ull);
+    s.ev[pos & s.ev_mask] = rec;
+    const unsigned b = (unsigned)((t + delay) & (WHEEL - 1));
+    atomicAdd(s.bnev + b, 1u);
+    if ((rec >> EV_LANE_BIT) & 1) atomicAdd(s.bnlane + b, 1u);
+    file_run(s, b, pos, 1u);
+  }
+}
+
 __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t) {
   const unsigned m = __ballot_sync(0xFFFFFFFFu, pred);
   if (m == 0) return;
@@ -50,19 +63,7 @@ __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long re
   unsigned base = 0;
   if ((int)lane == leader) base = atomicAdd(&sm.np, (unsigned)__popc(m));
   base = __shfl_sync(0xFFFFFFFFu, base, leader);
-  if (pred) {
-    const unsigned idx = base + __popc(m & ((1u << lane) - 1u));
-    if (idx < (unsigned)QP_CAP) {
-      sm.qp[idx] = rec | ((unsigned long long)delay << EV_DELAY_SHIFT);
-    } else {                        // rare: staging full, file the event as a run of one
-      const unsigned long long pos = atomicAdd(&s.ctl->ev_head, 1ull);
-      s.ev[pos & s.ev_mask] = rec;
-      const unsigned b = (unsigned)((t + delay) & (WHEEL - 1));
-      atomicAdd(s.bnev + b, 1u);
-      if ((rec >> EV_LANE_BIT) & 1) atomicAdd(s.bnlane + b, 1u);
-      file_run(s, b, pos, 1u);
-    }
-  }
+  if (pred) ev_stage(s, sm, base + __popc(m & ((1u << lane) - 1u)), rec, delay, t);
 }
 
 // Counting-sort the staged events by delay and append each delay's events to
@@ -74,12 +75,32 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
   if (n > 0) {
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.hist[d] = 0; sm.hlane[d] = 0; }
     __syncthreads();
+#if !WCSP_FLUSH_MATCH
     for (unsigned i = threadIdx.x; i < n; i += THREADS) {
       const unsigned long long e = sm.qp[i];
       const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
       sm.rank[i] = (unsigned short)atomicAdd(&sm.hist[d], 1u);
       if ((e >> EV_LANE_BIT) & 1) atomicAdd(&sm.hlane[d], 1u);
     }
+#else
+    const unsigned lane = threadIdx.x & 31u;
+    for (unsigned i0 = threadIdx.x & ~31u; i0 < n; i0 += THREADS) {   // warp-uniform trip count
+      const unsigned i = i0 + lane;
+      const bool valid = i < n;
+      const unsigned long long e = valid ? sm.qp[i] : 0ull;
+      const unsigned d = valid ? (unsigned)(e >> EV_DELAY_SHIFT) : 0xFFFFu;
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);      // lanes with the same delay
+      const int leader = __ffs(peers) - 1;
+      const unsigned lanes_in = __popc(peers & __ballot_sync(0xFFFFFFFFu, valid && ((e >> EV_LANE_BIT) & 1)));
+      unsigned base = 0;
+      if (valid && (int)lane == leader) {
+        base = atomicAdd(&sm.hist[d], (unsigned)__popc(peers));
+        if (lanes_in) atomicAdd(&sm.hlane[d], lanes_in);
+      }
+      base = __shfl_sync(0xFFFFFFFFu, base, leader);
+      if (valid) sm.rank[i] = (unsigned short)(base + __popc(peers & ((1u << lane) - 1u)));
+    }
+#endif
     __syncthreads();
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
       const unsigned cnt = sm.hist[d];
@@ -121,6 +142,9 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
 __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
   reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
   s.ctl->ts0 = globaltimer_ns();
+  if (s.staircase) s.ctl->n_barr = 0;   // staircase: target arrivals are resolved per cycle
+  unsigned long long* nf = &s.ctl->fin[(v.c + 1) & 1][0][0];
+  nf[0] = 0; nf[1] = 0; nf[2] = 0; nf[3] = 0;
   const unsigned prev = (unsigned)((v.t - v.delta) & (WHEEL - 1));   // the bucket fired last cycle
   s.bnev[prev] = 0; s.bnlane[prev] = 0;
   s.ctl->hist_t[v.c & (WHEEL - 1)] = v.t;
@@ -274,21 +298,42 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
         const unsigned long long t2 = globaltimer_ns();
         TraceRec r{v.t, (long long)v.delta, (long long)__ldcg(s.bndesc + (size_t)b * s.nblocks), pl, pp,
                    (long long)triggered, (long long)arrivals, new_p, (long long)relabels,
-                   (long long)__ldcg(&a->tested), (long long)(C->ts1 - C->ts0), (long long)(t2 - C->ts1)};
+                   (long long)__ldcg(&a->tested), (long long)(C->ts1 - C->ts0), (long long)(t2 - C->ts1),
+                   (long long)(C->fin[v.c & 1][0][0] - C->fin[v.c & 1][0][1] / s.nblocks),
+                   (long long)(C->fin[v.c & 1][1][0] - C->fin[v.c & 1][1][1] / s.nblocks)};
         s.trace[v.c - 1] = r;
       }
     }
     C->arrivals += arrivals; C->triggered += triggered; C->created += new_p; C->relabels += relabels;
     C->started += new_l;
   }
-  if (G.bhit) {
+  // staircase mode: a target arrival that beats every earlier one is a step of
+  // the F1*(M) staircase; the run goes on until nothing is live (or a step reaches f2_stop)
+  bool hit_stop = G.bhit != 0;
+  if (G.bhit && s.staircase) {
+    const long long q = (long long)((unsigned long long)G.bhit >> 32);
+    if (writer && q > C->stair_q) {
+      resolve_hit(s, (unsigned long long)G.bhit, v.t);
+      const unsigned k = C->n_stair;
+      if (k < s.stair_cap) {
+        s.stair[4 * k] = v.t;
+        s.stair[4 * k + 1] = C->F2;
+        s.stair[4 * k + 2] = C->X;
+        s.stair[4 * k + 3] = C->Y;
+      }
+      C->n_stair = k + 1;
+      C->stair_q = q;
+    }
+    hit_stop = (s.minf ? -1 : (long long)s.M - q) <= s.f2stop;
+  }
+  if (hit_stop) {
     nv.status = 0;
-    if (writer) resolve_hit(s, (unsigned long long)G.bhit, v.t);
+    if (writer && !s.staircase) resolve_hit(s, (unsigned long long)G.bhit, v.t);
   } else if (G.overflow) {
     nv.status = 8;  // WCSP_EOVERFLOW: the host grows the event ring / descriptor table and re-runs
     if (writer) C->need_pool = need;
   } else if (!G.pending) {
-    nv.status = 1;  // 2°: no live edge
+    nv.status = s.staircase && __ldcg(&C->n_stair) ? 0 : 1;  // 2°: no live edge
   } else if (s.budget > 0 && (long long)v.c >= s.budget) {
     nv.status = 4;
   } else {
@@ -404,19 +449,21 @@ __global__ void __launch_bounds__(THREADS, 4) k_wheel_persistent(Dev s) {
   while (v.status == ST_RUNNING) {
     if (v.c > 0) {
       if (blockIdx.x == 0 && threadIdx.x == 0) wheel_cycle_start(s, v);
+      if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
       wheel_fire<D>(s, v, sm);
       target += G;
-      if (!grid_sync(s.ctl, target, sm)) return;
+      if (!grid_sync(s.ctl, target, sm, &s.ctl->fin[v.c & 1][0][0])) return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
     if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
     __syncthreads();
     const unsigned long long bhit = sm.bhit;
     __syncthreads();
-    if (!bhit) {
+    if (!bhit || s.staircase) {
+      if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
       phase_treat<D, true>(s, v, sm);
       target += G;
-      if (!grid_sync(s.ctl, target, sm)) return;
+      if (!grid_sync(s.ctl, target, sm, &s.ctl->fin[v.c & 1][1][0])) return;
     }
     const View prev = v;
     if (threadIdx.x == 0) {
@@ -454,7 +501,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_wheel_treat(Dev s) {
   load_view(s, sm, v);
   if (v.status != ST_RUNNING) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
-  if (__ldcg(&s.ctl->acc[v.c % 3].bhit)) return;
+  if (__ldcg(&s.ctl->acc[v.c % 3].bhit) && !s.staircase) return;
   phase_treat<D, true>(s, v, sm);
 }
 

@@ -17,7 +17,7 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libwcsp.so")
+LIB_PATH = os.environ.get("WCSP_LIB") or os.path.join(_PKG, "libwcsp.so")   # WCSP_LIB: A/B builds
 
 M_INF = -1
 M_MAX = 65533
@@ -63,7 +63,7 @@ class _Result(ctypes.Structure):
 
 
 TRACE_FIELDS = ["t", "delta", "active_vertices", "live_lanes", "phantoms", "triggered", "arrivals",
-                "created", "relabels", "tested", "ns_arrive", "ns_treat"]
+                "created", "relabels", "tested", "ns_arrive", "ns_treat", "ns_arrive_spread", "ns_treat_spread"]
 
 
 class _TraceRec(ctypes.Structure):
@@ -71,7 +71,8 @@ class _TraceRec(ctypes.Structure):
 
 
 EXPORTS = ["wcsp_create", "wcsp_load", "wcsp_solve", "wcsp_set_targets", "wcsp_reconstruct", "wcsp_trace",
-           "wcsp_validate_path", "wcsp_destroy", "wcsp_last_error", "wcsp_version", "wcsp_nccl_unique_id"]
+           "wcsp_validate_path", "wcsp_destroy", "wcsp_last_error", "wcsp_version", "wcsp_nccl_unique_id",
+           "wcsp_staircase"]
 
 _lib = None
 
@@ -104,6 +105,9 @@ def load_library(path: str = LIB_PATH):
     lib.wcsp_destroy.restype = None
     lib.wcsp_last_error.restype = ctypes.c_char_p
     lib.wcsp_version.restype = ctypes.c_char_p
+    lib.wcsp_staircase.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), R]
+    lib.wcsp_staircase.restype = ctypes.c_int
     lib.wcsp_nccl_unique_id.argtypes = [ctypes.c_char_p]
     lib.wcsp_nccl_unique_id.restype = ctypes.c_int
     _lib = lib
@@ -256,6 +260,18 @@ class Solver:
         if st != REACHED:
             raise WcspError(st, last_error())
         return [int(buf[i]) for i in range(n.value)], _res(st, r)
+
+    def staircase(self, M_max: int, f2_stop: int = -(1 << 62), cap: int = 1 << 16):
+        """Every step (F1, F2, X, Y) of the F1*(M) staircase for budgets M <= M_max, in
+        one run (wcsp_staircase): the optimum for budget M is the first step with F2 < M."""
+        buf = (ctypes.c_int64 * (4 * cap))()
+        n = ctypes.c_int64(0)
+        r = _Result()
+        st = self._lib.wcsp_staircase(self._h, int(M_max), int(f2_stop), buf, cap, ctypes.byref(n), ctypes.byref(r))
+        if st not in (REACHED, INFEASIBLE):
+            raise WcspError(st, last_error())
+        m = min(n.value, cap)
+        return [tuple(int(buf[4 * i + k]) for k in range(4)) for i in range(m)], _res(st, r)
 
     def trace(self) -> dict:
         """Per-cycle counters of the last solve: dict of numpy int64 arrays."""

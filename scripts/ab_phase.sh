@@ -1,0 +1,7 @@
+#!/bin/bash
+# A/B: per-phase breakdown of libwcsp.so variants (WCSP_LIB) on one workload
+W=${W:-C3}
+for v in base ${VARIANTS}; do
+  if [ "$v" = base ]; then lib=paper_1511_06441_b200/libwcsp.so; else lib=paper_1511_06441_b200/libwcsp_$v.so; fi
+  echo "== $v"; WCSP_L2_PERSIST=0 WCSP_LIB=$lib python scripts/phase_breakdown.py $W wheel 2>&1 | grep '"cycle_ms"'
+done

@@ -22,7 +22,9 @@ for e in engines:
     out[e] = {"cycle_ms": r.cycle_ms, "cycles": r.cycles, "arrive_ms": na, "treat_ms": nt,
               "other_ms": r.cycle_ms - na - nt, "tested": int(tr["tested"].sum()), "triggered": r.triggered,
               "arrivals": r.arrivals, "created": r.phantoms_created, "started": r.lanes_started,
-              "max_cycle_us": float((tr["ns_arrive"] + tr["ns_treat"]).max() / 1e3)}
+              "max_cycle_us": float((tr["ns_arrive"] + tr["ns_treat"]).max() / 1e3),
+              "arrive_spread_ms": float(tr["ns_arrive_spread"][1:].sum() / 1e6),
+              "treat_spread_ms": float(tr["ns_treat_spread"][1:].sum() / 1e6)}
     print(wl, e, json.dumps(out[e]), flush=True)
     if e.startswith("wheel"):
         nd = tr["active_vertices"].astype(float)

@@ -311,3 +311,30 @@ def test_slab_engine_nccl_single_rank():
             rn = s.solve()
         assert rn.key() == r1.key()
         assert (rn.edge_updates, rn.cycles, rn.phantoms_created) == (r1.edge_updates, r1.cycles, r1.phantoms_created)
+
+
+@pytest.mark.parametrize("engine", ["wheel", "wheel_stepped"])
+def test_staircase_every_budget_in_one_run(engine):
+    """one run at M_max records the whole F1*(M) staircase; for
+    every budget M <= M_max the oracle's optimum is the first step
+    with F2 < M (X and Y included), infeasible below the last step."""
+    rng = np.random.default_rng(808)
+    checked = 0
+    for i in range(25):
+        inst = I.random_small(rng, shapes=[(8, 8), (10, 7), (5, 4, 3), (12, 12)], M_range=(1, 1),
+                              max_sources=3, max_targets=3)
+        hi = oracle.solve_lex(inst, 0)
+        if hi.status != oracle.REACHED:
+            continue
+        M_max = hi.F2 + 4
+        with wcsp.Solver(inst.with_M(M_max), engine=engine) as s:
+            steps, r = s.staircase(M_max)
+        assert steps and all(a[0] < b[0] and a[1] > b[1] for a, b in zip(steps, steps[1:]))
+        assert steps[0][:2] == (hi.F1, hi.F2)        # the unconstrained (lexicographic) optimum first
+        for M in range(1, M_max + 1):
+            o = oracle.solve_pruned(inst.with_M(M))
+            st = next((x for x in steps if x[1] < M), None)
+            want = (oracle.INFEASIBLE,) if st is None else (oracle.REACHED,) + tuple(st)
+            assert o.key() == want, (inst.shape, M, steps, o)
+            checked += 1
+    assert checked > 300

@@ -40,6 +40,11 @@ WORKLOADS = {
     "C4": {"shape": None, "desc": "configs[3]: Theorem-2 fractal omega_k, k = 10 (t = 1024), V = [-t,t]x[0,t+1], "
                                   "A = x-axis, B = (0,t), f1 in {1,2}, f2 = 1, M = infinity"},
 }
+for _side in (50, 75, 100, 125):   # the §6 protocol: water on the boundary, B = centre
+    WORKLOADS[f"P6-{_side}"] = {"shape": (_side,) * 3, "desc": f"§6 cube {_side}^3, boundary -> centre, "
+                                                             f"f1,f2 ~ U{{1..10}}, M = M_bind"}
+    WORKLOADS[f"P6-{_side}-inf"] = {"shape": (_side,) * 3, "desc": f"§6 cube {_side}^3, boundary -> centre, "
+                                                                 f"f1 ~ U{{1..10}}, M = infinity"}
 MBIND = os.path.join(ROOT, "paper_1511_06441_b200", "data", "mbind.json")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "roofline_traffic.json")
 
@@ -54,6 +59,11 @@ def workload_instance(name: str, seed: int):
         inst = I.fractal_instance(10)
         return inst, {"seed": 0, "F1_lex": 1024, "M_bind": I.M_INF}
     table = json.load(open(MBIND))
+    if name.startswith("P6-"):
+        base = name[:-4] if name.endswith("-inf") else name
+        meta = dict(table[f"{base}/0"])
+        M = I.M_INF if name.endswith("-inf") else meta["M_bind"]
+        return I.grid_instance(WORKLOADS[name]["shape"], 0, 1, 10, "boundary", "centre", M, name), meta
     key = f"{name}/{seed}"
     if key not in table:
         key = f"{name}/0"
@@ -310,9 +320,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r, dt, t_limit = cpu_sample(inst)
+        import oracle
+        what = (f"the first {t_limit} time units of the same instance" if r.status == oracle.ELIMIT
+                else "the whole instance")
         cpu = {"value": r.work / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"oracle tier 2 (oracle/wcsp_oracle.c orc_pruned) on the first {t_limit} time units of the "
-                         f"same instance ({dt:.1f} s, {r.work} flow-updates, {r.cycles} event times)"}
+               "sample": f"oracle tier 2 (oracle/wcsp_oracle.c orc_pruned) on {what} "
+                         f"({dt:.2f} s, {r.work} flow-updates, {r.cycles} event times)"}
 
     if rank == 0:
         line = {

@@ -16,7 +16,9 @@ import oracle  # noqa: E402
 from paper_1511_06441_b200 import instances as I  # noqa: E402
 
 OUT = os.path.join(ROOT, "paper_1511_06441_b200", "data", "mbind.json")
-SHAPES = {"C2": (1024, 1024), "C3": (256, 256, 256), "C3s": (128, 128, 128)}
+SHAPES = {"C2": (1024, 1024), "C3": (256, 256, 256), "C3s": (128, 128, 128),
+          # §6 protocol: water on the cube's boundary, B = the centre vertex
+          "P6-50": (50, 50, 50), "P6-75": (75, 75, 75), "P6-100": (100, 100, 100), "P6-125": (125, 125, 125)}
 
 
 def main():
@@ -33,7 +35,10 @@ def main():
             if key in table:
                 continue
             t0 = time.time()
-            inst = I.config_face(SHAPES[name], seed, I.M_INF)
+            if name.startswith("P6"):
+                inst = I.grid_instance(SHAPES[name], seed, 1, 10, "boundary", "centre", I.M_INF, name)
+            else:
+                inst = I.config_face(SHAPES[name], seed, I.M_INF)
             lo, hi = oracle.solve_lex(inst, 1), oracle.solve_lex(inst, 0)
             table[key] = {"shape": list(SHAPES[name]), "seed": seed, "F2_min": lo.F2, "F1_at_F2min": lo.F1,
                           "F2_lex": hi.F2, "F1_lex": hi.F1, "M_bind": (lo.F2 + hi.F2) // 2 + 1,

@@ -10,9 +10,10 @@ holding no arithmetic of the method).
 Tiers (see wcsp_oracle.c): dense (definition on the product graph, PAPER.md
 :13-21), pruned (time-ordered label setting on remaining quality),
 lex (Dijkstra with lexicographic keys: the M endpoints and M = infinity),
-brute (simple-path enumeration).  Parity status: all four pinned by
+brute (simple-path enumeration), model (the paper's nine-step cycle run
+sequentially, also counting its work).  Parity status: all five pinned by
 tests/test_oracle.py (brute force, closed forms P3/P4, monotonicity P5,
-fixtures B/D, counts P9).
+fixtures B/D, counts P9, hand-traced cycle counts of fixture B).
 """
 from __future__ import annotations
 
@@ -53,6 +54,11 @@ class _Result(ctypes.Structure):
                 ("cycles", ctypes.c_int64), ("t_reached", ctypes.c_int64)]
 
 
+class _Counters(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in
+                ("cycles", "work", "arrivals", "triggered", "created", "started", "relabels")]
+
+
 _lib = None
 
 
@@ -68,6 +74,10 @@ def _load():
         lib.orc_pruned.restype = ctypes.c_int
         lib.orc_lex.argtypes = [ctypes.POINTER(_Problem), ctypes.c_int, ctypes.POINTER(_Result)]
         lib.orc_lex.restype = ctypes.c_int
+        lib.orc_model.argtypes = [ctypes.POINTER(_Problem), ctypes.c_int, ctypes.POINTER(_Result),
+                                  ctypes.POINTER(_Counters), ctypes.c_void_p, ctypes.c_int64,
+                                  ctypes.POINTER(ctypes.c_int64)]
+        lib.orc_model.restype = ctypes.c_int
         lib.orc_validate_path.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(ctypes.c_int64),
                                           ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
                                           ctypes.POINTER(ctypes.c_int64)]
@@ -147,6 +157,41 @@ def solve_brute(inst) -> Result:
     r = _Result()
     _load().orc_brute(ctypes.byref(p), ctypes.byref(r))
     return _res(r)
+
+
+@dataclasses.dataclass
+class Counters:
+    """Work of the method's cycle (tier 5): cycles, sum of live edges + phantoms over
+    cycles (work, the north_star numerator), arrivals, triggered vertices, phantoms
+    created, lanes started, relabels; the initial treatment of A (t = 0) included."""
+    cycles: int
+    work: int
+    arrivals: int
+    triggered: int
+    created: int
+    started: int
+    relabels: int
+
+
+def solve_model(inst, unit: bool = False, events: int = 0):
+    """Tier 5: the paper's nine-step cycle run sequentially -> (Result, Counters), plus,
+    if events > 0, the first `events` events as a list of dicts {t, kind, v, u, label}:
+    "relabel" (v relabelled to label at t), "phantom" (created at t by v toward u,
+    label = L* of v), "cycle" (advancing to t: v = active vertices, u = live
+    edges, label = live phantoms at the top of the cycle)."""
+    p, keep = _problem(inst)
+    r = _Result()
+    c = _Counters()
+    ev = np.zeros((max(events, 1), 5), dtype=np.int64)
+    n = ctypes.c_int64(0)
+    _load().orc_model(ctypes.byref(p), 1 if unit else 0, ctypes.byref(r), ctypes.byref(c),
+                      ev.ctypes.data if events > 0 else None, int(events), ctypes.byref(n))
+    out = (_res(r), Counters(*[int(getattr(c, nm)) for nm, _ in _Counters._fields_]))
+    if events <= 0:
+        return out
+    log = [dict(t=int(e[0]), kind=("relabel", "phantom", "cycle")[int(e[1])], v=int(e[2]), u=int(e[3]),
+                label=int(e[4])) for e in ev[:min(n.value, events)]]
+    return out + (log,)
 
 
 def solve(inst) -> Result:

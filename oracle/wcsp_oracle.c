@@ -13,6 +13,9 @@
  *   tier 3 orc_lex    — Dijkstra with lexicographic keys (the two M endpoints,
  *                       SURVEY §8(c) P4, and M = infinity).
  *   tier 4 orc_brute  — enumeration of simple paths (tiny graphs).
+ *   tier 5 orc_model  — the paper's own cycle (§4) run sequentially,
+ *                       one vertex and one edge at a time; it also counts the
+ *                       method's work (the north_star metric's numerator).
  */
 #include "wcsp_oracle.h"
 
@@ -451,4 +454,184 @@ int orc_validate_path(const orc_problem* p, const int64_t* path, int64_t len, in
   *F2 = s2;
   if (p->M != ORC_M_INF && s2 >= p->M) return ORC_INFEASIBLE;
   return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Tier 5: the nine-step cycle of PAPER.md §4, one vertex / edge at a time.  */
+/* State: label L(v), the residual time of each half-edge     */
+/* (v, j) that carries v's water (the active edges; 0 = idle),  */
+/* the phantom edges (src, lane, quality, residual), the  */
+/* temporary labels of this cycle and the triggered set.      */
+/* ------------------------------------------------------------------------- */
+
+typedef struct { int64_t src; int lane; int32_t cand; int32_t res; } phantom;
+
+static void log_event(orc_event* ev, int64_t cap, int64_t* n, int64_t t, int64_t kind, int64_t v,
+                      int64_t u, int64_t label) {
+  if (ev && *n < cap) { ev[*n].t = t; ev[*n].kind = kind; ev[*n].v = v; ev[*n].u = u; ev[*n].label = label; }
+  if (ev) ++*n;
+}
+
+int orc_model(const orc_problem* p, int unit, orc_result* r, orc_counters* cnt,
+              orc_event* ev, int64_t ev_cap, int64_t* n_ev) {
+  int64_t nev_ = 0;
+  if (!n_ev) n_ev = &nev_;
+  *n_ev = 0;
+  memset(r, 0, sizeof(*r));
+  memset(cnt, 0, sizeof(*cnt));
+  if (check_problem(p)) return (int)(r->status = ORC_EINVAL);
+  grid g;
+  grid_init(&g, p);
+  const int64_t N = g.N;
+  const int NL = 2 * p->d;
+  const int minf = p->M == ORC_M_INF;
+  const int32_t M = minf ? 1 : (int32_t)p->M;
+  int32_t* L = (int32_t*)calloc((size_t)N, sizeof(int32_t));
+  int32_t* temp = (int32_t*)calloc((size_t)N, sizeof(int32_t));
+  uint8_t* trig = (uint8_t*)calloc((size_t)N, 1);
+  int32_t* res = (int32_t*)calloc((size_t)N * NL, sizeof(int32_t));
+  int64_t* tlist = (int64_t*)malloc((size_t)N * sizeof(int64_t));
+  phantom* ph = NULL;
+  int64_t nph = 0, cph = 0, t = 0;
+  if (!L || !temp || !trig || !res || !tlist) { r->status = ORC_ENOMEM; goto out; }
+
+  /* lane j of v: 2k -> v + e_k, 2k+1 -> v - e_k; its (f1, f2), or f1 = 0 if absent */
+#define LANE(v, j, U, F1, F2)                                                              \
+  do {                                                                                     \
+    const int k_ = (j) / 2;                                                                \
+    const int64_t xk_ = ((v) / g.stride[k_]) % g.n[k_];                                    \
+    F1 = 0; F2 = 0; U = -1;                                                                \
+    if (((j) & 1) == 0 && xk_ + 1 < g.n[k_]) {                                             \
+      U = (v) + g.stride[k_]; F1 = p->f1[k_ * N + (v)]; F2 = p->f2[k_ * N + (v)];          \
+    } else if (((j) & 1) == 1 && xk_ > 0) {                                                \
+      U = (v) - g.stride[k_]; F1 = p->f1[k_ * N + U]; F2 = p->f2[k_ * N + U];              \
+    }                                                                                      \
+    if (U >= 0 && (!is_present(&g, (v)) || !is_present(&g, U))) F1 = 0;                   \
+    if (minf) F2 = 0;                                                                      \
+  } while (0)
+
+  /* Steps 4, 5 and 8.1 for the triggered vertices in tlist[0..nt) */
+  int64_t nt = 0;
+  /* initial state: A triggered with temporary label M (reading R20) */
+  for (int64_t a = 0; a < N; ++a)
+    if (inA(&g, a) && !inB(&g, a)) { temp[a] = M; trig[a] = 1; tlist[nt++] = a; }
+  for (;;) {
+    /* ---- treat the triggered vertices (skipped in the terminating cycle) ---- */
+    for (int64_t i = 0; i < nt; ++i) {
+      const int64_t q = tlist[i];
+      const int32_t lstar = temp[q];
+      if (!(lstar > L[q])) continue;
+      cnt->triggered++;
+      int inactive = 1;                                   /* no live edge left (reading R6) */
+      for (int j = 0; j < NL; ++j) if (res[q * NL + j] > 0) inactive = 0;
+      for (int j = 0; j < NL; ++j) {
+        int64_t u; int a1, a2;
+        LANE(q, j, u, a1, a2);
+        if (a1 == 0) continue;
+        const int32_t c = lstar - a2;
+        const int32_t tu = trig[u] ? temp[u] : 0;        /* this cycle's temporary label only */
+        const int32_t lu = L[u] > tu ? L[u] : tu;
+        if (!(c > 0 && c > lu)) continue;                /* edge j triggered */
+        if (inactive) {                                  /* restart with time f1 */
+          res[q * NL + j] = a1;
+          cnt->started++;
+        } else {                                         /* phantom */
+          if (nph == cph) {
+            cph = cph ? 2 * cph : 1024;
+            phantom* np = (phantom*)realloc(ph, (size_t)cph * sizeof(phantom));
+            if (!np) { r->status = ORC_ENOMEM; goto out; }
+            ph = np;
+          }
+          ph[nph].src = q; ph[nph].lane = j; ph[nph].cand = c; ph[nph].res = a1;
+          ++nph;
+          cnt->created++;
+          log_event(ev, ev_cap, n_ev, t, 1, q, u, lstar);
+        }
+      }
+      if (inactive) {                                    /* Step 8.1: relabel */
+        L[q] = lstar;
+        cnt->relabels++;
+        log_event(ev, ev_cap, n_ev, t, 0, q, -1, lstar);
+      }
+    }
+    for (int64_t i = 0; i < nt; ++i) { trig[tlist[i]] = 0; temp[tlist[i]] = 0; }
+    nt = 0;
+    /* ---- Step 6, 2°: nothing live -> infeasible ---- */
+    int64_t live_e = 0, active_v = 0;
+    int32_t dmin = INT32_MAX;
+    for (int64_t v = 0; v < N; ++v) {
+      int act = 0;
+      for (int j = 0; j < NL; ++j) {
+        const int32_t rr = res[v * NL + j];
+        if (rr > 0) { ++live_e; act = 1; if (rr < dmin) dmin = rr; }
+      }
+      active_v += act;                                   /* active vertex */
+    }
+    for (int64_t i = 0; i < nph; ++i) if (ph[i].res < dmin) dmin = ph[i].res;
+    if (live_e + nph == 0) { r->status = ORC_INFEASIBLE; break; }
+    /* ---- Step 1: advance time (jump by the min residual) ---- */
+    const int32_t delta = unit ? 1 : dmin;
+    t += delta;
+    cnt->cycles++;
+    cnt->work += live_e + nph;
+    log_event(ev, ev_cap, n_ev, t, 2, active_v, live_e, nph);
+    /* ---- Steps 1-3: edges and phantoms reaching 0 deliver their water ---- */
+    int32_t bq = 0;
+    int64_t bx = -1, by = -1;
+    /* at B: keep the lexicographic best (quality desc, X asc, source asc), reading R5 */
+#define ARRIVE(D, CAND, SRC)                                                             \
+    do {                                                                                 \
+      const int64_t d_ = (D); const int32_t c_ = (CAND); const int64_t s_ = (SRC);       \
+      if (c_ > 0) {                                                                      \
+        if (inB(&g, d_)) {                         /* 1°: a vertex of B */ \
+          if (c_ > bq || (c_ == bq && d_ < bx)) { bq = c_; bx = d_; by = s_; }           \
+          else if (c_ == bq && d_ == bx && s_ < by) by = s_;                             \
+        } else if (c_ > L[d_]) {                   /* PAPER.md:32 */                     \
+          if (!trig[d_]) { trig[d_] = 1; tlist[nt++] = d_; temp[d_] = c_; }              \
+          else if (c_ > temp[d_]) temp[d_] = c_;                                         \
+        }                                                                                \
+      }                                                                                  \
+    } while (0)
+    for (int64_t v = 0; v < N; ++v) {
+      for (int j = 0; j < NL; ++j) {
+        int32_t* rr = &res[v * NL + j];
+        if (*rr <= 0) continue;
+        *rr -= delta;
+        if (*rr == 0) {
+          int64_t u; int a1, a2;
+          LANE(v, j, u, a1, a2);
+          (void)a1;
+          cnt->arrivals++;
+          ARRIVE(u, L[v] - a2, v);
+        }
+      }
+    }
+    int64_t keep = 0;
+    for (int64_t i = 0; i < nph; ++i) {
+      ph[i].res -= delta;
+      if (ph[i].res == 0) {
+        int64_t u; int a1, a2;
+        LANE(ph[i].src, ph[i].lane, u, a1, a2);
+        (void)a1; (void)a2;
+        cnt->arrivals++;
+        ARRIVE(u, ph[i].cand, ph[i].src);
+      } else {
+        ph[keep++] = ph[i];                             /* Step 7 */
+      }
+    }
+    if (bx >= 0) {                                       /* terminate in this cycle (R17) */
+      r->status = ORC_REACHED;
+      r->F1 = t; r->F2 = minf ? -1 : M - bq; r->X = bx; r->Y = by;
+      break;
+    }
+    nph = keep;
+  }
+#undef ARRIVE
+#undef LANE
+out:
+  r->work = cnt->work;
+  r->cycles = cnt->cycles;
+  r->t_reached = t;
+  free(L); free(temp); free(trig); free(res); free(tlist); free(ph);
+  return (int)r->status;
 }

@@ -52,6 +52,24 @@ int orc_pruned(const orc_problem* p, int64_t t_limit, orc_result* r);
 int orc_lex(const orc_problem* p, int mode, orc_result* r);
 /* Tier 4: exhaustive simple-path enumeration (tiny graphs only, N <= 24). */
 int orc_brute(const orc_problem* p, orc_result* r);
+/* Tier 5: the paper's cycle simulated step by step, sequentially (§4,
+ * :155-227, in the SURVEY §8(a) canonical form: 'post' activeness R6, no twin
+ * demotion R8, no eager kill R7, jump or unit time R4).  Outputs as tier 1; it
+ * also counts the method's work: cycles, sum over cycles of live edges + live
+ * phantoms (work), arrivals (edges/phantoms whose time reached 0), triggered
+ * vertices (accepted first arrivals), phantoms created, lanes started,
+ * relabels.  unit = 1: advance by 1; 0: by the min residual. */
+typedef struct {
+  int64_t cycles, work, arrivals, triggered, created, started, relabels;
+} orc_counters;
+/* Optional event log (ev may be NULL): kind 0 = relabel of v to `label` at t
+ * (Step 8.1), kind 1 = phantom created at t by v toward u carrying the label
+ * `label` = L* of v (Step 5; the water it delivers is label - f2),
+ * kind 2 = a cycle advancing to t: v = active vertices (>= 1 live edge) and
+ * u = live edges at its top, label = live phantoms. */
+typedef struct { int64_t t, kind, v, u, label; } orc_event;
+int orc_model(const orc_problem* p, int unit, orc_result* r, orc_counters* cnt,
+              orc_event* ev, int64_t ev_cap, int64_t* n_ev);
 /* Path check (PAPER.md:13-18 definitions of path, F1, F2). Returns 0 if path is
  * an A->B path over present edges with F2 < M; writes F1, F2. */
 int orc_validate_path(const orc_problem* p, const int64_t* path, int64_t len, int64_t* F1, int64_t* F2);

@@ -1,9 +1,10 @@
 """Parity of the CUDA path (through the C-ABI) with the CPU oracle (-m gpu).
 
-Bar: integer outputs (status, F1, F2, X, Y) bit-exact;
-the work counters (cycles, edge_updates = sum over cycles of live edges +
-phantoms)
-bound the oracle's tier-2 counters from above (see check()).
+Bar: integer outputs (status, F1, F2, X, Y) bit-exact
+with the oracle; the work counters (cycles, edge_updates = sum over cycles of
+live edges + phantoms, arrivals, triggered, phantoms created, lanes started,
+relabels) bit-exact with oracle tier 5, the paper's cycle run sequentially
+(see check()).
 """
 import json
 import os
@@ -21,18 +22,29 @@ GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fixture
 ENGINES = ["persistent", "stepped", "wheel", "wheel_stepped"]
 
 
-def check(inst, engine="persistent", time_mode="jump", counters=True, want=None):
-    r = wcsp.solve(inst, engine=engine, time_mode=time_mode)
+MODEL_MAX_CELLS = 40_000_000     # N * cycles the sequential model (tier 5) runs in seconds
+
+
+def model_counters(r):
+    return (r.cycles, r.edge_updates, r.arrivals, r.triggered, r.phantoms_created, r.lanes_started,
+            r.relabels)
+
+
+def check(inst, engine="persistent", time_mode="jump", counters=True, want=None, **kw):
+    """Outputs bit-exact with oracle tier 2; with counters=True also the work
+    counters bit-exact with tier 5, the paper's cycle run sequentially
+    (cycles, edge_updates = sum over cycles of live edges + phantoms, arrivals,
+    triggered, phantoms created, lanes started, relabels)."""
+    r = wcsp.solve(inst, engine=engine, time_mode=time_mode, **kw)
     o = oracle.solve_pruned(inst)
     assert r.key() == o.key(), (inst.name, inst.seed, inst.shape, inst.M, r, o)
     if want is not None:
         assert r.key() == want.key()
-    if counters and time_mode == "jump":
-        # The oracle keeps the best quality ever seen at a vertex; the method keeps an
-        # active vertex's label unchanged so it may accept (and re-send)
-        # water between L and that best.  Its flows are therefore a superset of the
-        # oracle's events: never less work, never fewer event times.
-        assert r.cycles >= o.cycles and r.edge_updates >= o.work, (inst.name, r, o)
+    if counters:
+        m, mc = oracle.solve_model(inst, unit=time_mode == "unit")
+        assert m.key() == r.key()
+        assert model_counters(r) == (mc.cycles, mc.work, mc.arrivals, mc.triggered, mc.created,
+                                     mc.started, mc.relabels), (inst.name, inst.shape, inst.M, r, mc)
     return r, o
 
 
@@ -50,6 +62,16 @@ def test_mechanism_fixtures(name, engine):
     t_created = tr["t"][tr["created"] > 0]
     assert list(t_created) == [ev["t"]]
     assert r.phantoms_created == 1
+    # the whole hand trace of the §4 steps (tests/golden 'hand_trace', pinned in test_oracle.py)
+    ht = GOLD[name]["hand_trace"]
+    got = [[int(t), int(a), int(e), int(p)] for t, a, e, p in
+           zip(tr["t"], tr["active_vertices"], tr["live_lanes"], tr["phantoms"])]
+    if engine.startswith("wheel"):   # the wheel keeps no active-vertex list (trace slot reused)
+        got = [[x[0], h[1], x[2], x[3]] for x, h in zip(got, ht["cycles"])]
+    assert got == ht["cycles"]
+    hc = ht["counters"]
+    assert model_counters(r) == (hc["cycles"], hc["work"], hc["arrivals"], hc["triggered"], hc["created"],
+                                 hc["started"], hc["relabels"])
     # every narrated relabel time is a cycle of the run (jump mode visits exactly these times)
     for x in GOLD[name]["events"]:
         assert x["t"] in set(tr["t"].tolist())
@@ -89,8 +111,8 @@ def test_unit_equals_jump():
     rng = np.random.default_rng(303)
     for i in range(60):
         inst = I.random_small(rng, shapes=[(10, 10), (5, 5, 5)], M_range=(5, 80))
-        rj = wcsp.solve(inst, time_mode="jump")
-        ru = wcsp.solve(inst, time_mode="unit")
+        rj, _ = check(inst, time_mode="jump")
+        ru, _ = check(inst, time_mode="unit")
         assert rj.key() == ru.key()
         if rj.status == wcsp.REACHED:
             assert ru.cycles == rj.F1   # unit mode visits every t = 1..F1

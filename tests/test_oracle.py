@@ -13,6 +13,7 @@ Each check ties the oracle to something other than itself (SURVEY §8(c)
   * the §5 Lemma proof's first-passage times on the speedway
         (PAPER.md:270-279): tau(x, y) = y + min(y, 2|x|).
 """
+import dataclasses
 import json
 import os
 
@@ -328,3 +329,89 @@ def test_fractal_closed_form_P7():
             assert len(I.fractal_fast_edges(k)) > len(prev)
             assert all(abs(x) <= t and 0 <= y <= t for e in I.fractal_fast_edges(k) for (x, y) in e)
             assert scale  # (the scaled previous level is a different lattice; only monotonicity in k is asserted)
+
+
+# ---------------------------------------------------------------------------
+# tier 5: the paper's cycle run sequentially (oracle.solve_model)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["fixtureB", "fixtureD"])
+def test_model_hand_trace_and_narrated_events(name):
+    """The model reproduces, cycle by cycle, the hand trace of the §4 steps on
+    the mechanism fixtures (golden 'hand_trace'), and every event the paper
+    narrates for that mechanism (relabel times and labels, the
+    phantom's time, endpoints and label)."""
+    g = GOLD[name]
+    inst = getattr(I, "fixture_" + name[-1])()
+    r, c, log = oracle.solve_model(inst, events=1000)
+    e = g["expect"]
+    assert r.key() == (oracle.REACHED, e["F1"], e["F2"], e["X"], e["Y"])
+    ht = g["hand_trace"]
+    assert [[x["t"], x["v"], x["u"], x["label"]] for x in log if x["kind"] == "cycle"] == ht["cycles"]
+    assert dataclasses.asdict(c) == ht["counters"]
+    relabels = {(x["t"], x["v"], x["label"]) for x in log if x["kind"] == "relabel"}
+    phantoms = {(x["t"], x["v"], x["u"], x["label"]) for x in log if x["kind"] == "phantom"}
+    for ev in g["events"]:
+        if "phantom_from" in ev:
+            assert (ev["t"], inst.index(tuple(ev["phantom_from"])), inst.index(tuple(ev["phantom_to"])),
+                    ev["phantom_label"]) in phantoms
+        else:
+            assert (ev["t"], inst.index(tuple(ev["vertex"])), ev["label"]) in relabels
+
+
+def test_model_outputs_vs_brute_and_dense():
+    """Tier 5's outputs are the optimum (reading R5 tie-break) in
+    jump and unit time (reading R4)."""
+    for inst in tiny_instances(200, 14):
+        b = oracle.solve_brute(inst).key()
+        assert oracle.solve_model(inst)[0].key() == b, inst
+        assert oracle.solve_model(inst, unit=True)[0].key() == b, inst
+    for inst in mid_instances(80, 15):
+        assert oracle.solve_model(inst)[0].key() == oracle.solve_pruned(inst).key(), inst
+
+
+def test_model_unit_vs_jump_counters():
+    """Reading R4: advancing by 1 instead of by the minimum
+    residual only inserts idle cycles: the same arrivals,
+    triggerings, phantoms, starts and relabels; unit mode visits every
+    t = 1..F1; the idle cycles only add work."""
+    for inst in mid_instances(60, 16):
+        rj, cj = oracle.solve_model(inst)
+        ru, cu = oracle.solve_model(inst, unit=True)
+        assert rj.key() == ru.key()
+        same = ("arrivals", "triggered", "created", "started", "relabels")
+        assert [getattr(cj, k) for k in same] == [getattr(cu, k) for k in same]
+        assert cu.cycles >= cj.cycles and cu.work >= cj.work
+        if rj.status == oracle.REACHED:
+            assert cu.cycles == rj.F1
+
+
+def test_model_counter_identities():
+    """Every arrival is a started edge or a created phantom (PAPER.md:190-198);
+    every triggered vertex is relabelled or spawns only phantoms (Step 8.1,
+    PAPER.md:211); M = inf never creates a phantom (an active vertex's first
+    arrival is already its best)."""
+    for inst in mid_instances(60, 17):
+        r, c = oracle.solve_model(inst)
+        assert c.arrivals <= c.started + c.created
+        assert c.relabels <= c.triggered
+        assert c.work >= c.arrivals
+        ri, ci = oracle.solve_model(inst.with_M(I.M_INF))
+        assert ci.created == 0
+
+
+def test_model_speedway_active_sequence():
+    """§5 Lemma environment, unit time, M = inf: the model's
+    active-vertex count at the top of cycle T + 1 equals the lazy active set at
+    T computed from first-passage times (reading R15, test_speedway_lemma_corrected)."""
+    n = 48
+    s = I.speedway_instance(n)
+    tau = first_passage(s)
+    r, c, log = oracle.solve_model(s, unit=True, events=10000)
+    assert r.F1 == n
+    cyc = [x for x in log if x["kind"] == "cycle"]
+    assert [x["t"] for x in cyc] == list(range(1, n + 1))
+    for x in cyc:
+        T = x["t"] - 1
+        if T >= 1:
+            assert x["v"] == len(speedway_sets(n, T, tau, s)[1]), T

@@ -218,6 +218,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--partition", default="replicas", choices=["replicas", "slabs"],
                     help="N > 1: independent seeds per rank (weak) or one instance cut into z-slabs (strong)")
+    ap.add_argument("--halo", default="peer", choices=["copy", "peer"],
+                    help="slab boundary: fused over peer memory in one kernel (peer) or ghost-plane copies")
+    ap.add_argument("--vslabs", type=int, default=0,
+                    help="N = 1: cut the instance into this many virtual slabs on the one GPU")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -236,7 +240,9 @@ def main():
     stream = torch.cuda.current_stream()
     if slabs:   # one instance, slab `rank` of `world` on this GPU, NCCL exchange every cycle
         solver = wcsp.Solver(inst, engine="wheel", stream=stream, nranks=world, rank=rank,
-                             nccl_id=share_nccl_id(rank))
+                             nccl_id=share_nccl_id(rank), halo=args.halo)
+    elif args.vslabs > 1:
+        solver = wcsp.Solver(inst, engine="wheel", stream=stream, slabs=args.vslabs, halo=args.halo)
     else:
         solver = wcsp.Solver(inst, engine=args.engine, stream=stream)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > L2 (126 MB)
@@ -293,7 +299,7 @@ def main():
 
     # e2e through the C-ABI with host buffers (pinned): H2D of the step's inputs + solve + result read
     e2e = None
-    if args.e2e_steps > 0 and not slabs:
+    if args.e2e_steps > 0 and not slabs and args.vslabs <= 1:
         pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(inst, k))).pin_memory()
                for k in ("f1", "f2", "maskA", "maskB")}
         host = {k: v.numpy() for k, v in pin.items()}
@@ -336,9 +342,12 @@ def main():
                        "shape": list(inst.shape), "seed": meta["seed"], "M": inst.M,
                        "M_bind_from": "paper_1511_06441_b200/data/mbind.json (oracle, scripts/make_mbind.py)",
                        "engine": args.engine, "l2": "flushed between steps (256 MiB write outside the events)",
-                       "parallelism": (f"{world} z-slabs of one instance (NCCL send/recv + allreduce per cycle)"
+                       "parallelism": (f"{world} z-slabs of one instance ("
+                                       + ("boundary fused over NVLink peer memory, one kernel per GPU"
+                                          if args.halo == "peer" else "NCCL send/recv + allreduce per cycle") + ")"
                                        if slabs else f"{world} independent instances (one seed per rank)")
-                                      if world > 1 else "1 GPU"},
+                                      if world > 1 else (f"1 GPU, {args.vslabs} virtual z-slabs ({args.halo} halo)"
+                                                         if args.vslabs > 1 else "1 GPU")},
             "solve_ms": total_ms / args.steps,
             "solve": {"F1": r0.F1, "F2": r0.F2, "X": r0.X, "Y": r0.Y, "cycles": r0.cycles,
                       "edge_updates": r0.edge_updates, "arrivals": r0.arrivals, "triggered": r0.triggered,

@@ -68,6 +68,8 @@ enum { WCSP_ENGINE_PERSISTENT = 0,   /* sweep engine: residual countdown on the 
        WCSP_ENGINE_WHEEL = 2,        /* timing-wheel engine: live edges stored by arrival time, written
                                         once and read once (same outputs and counters), persistent */
        WCSP_ENGINE_WHEEL_STEPPED = 3 };
+enum { WCSP_HALO_COPY = 0,          /* slab boundary: ghost planes exchanged by copies / NCCL per cycle */
+       WCSP_HALO_PEER = 1 };        /* slab boundary: fused into the cycle kernel over peer memory (f2) */
 
 /* Problem statement.  Validation (wcsp_create / wcsp_load):
  *  d in 1..4, every shape[k] >= 1, N <= 2^30;  A and B non-empty among the
@@ -101,7 +103,17 @@ typedef struct {
                                into `slabs` slabs with ghost planes that exchange the water crossing
                                a slab boundary every cycle (the multi-GPU layout run
                                on one GPU); requires engine WHEEL and host arrays.  0/1 = off. */
-  int32_t reserved0;
+  int32_t halo;             /* how slabs exchange their boundary (slabs > 1 or nranks > 1):
+                               WCSP_HALO_COPY (0, default): ghost planes, one copy / ncclSend-Recv
+                               of boundary water and labels per cycle, host-driven per-phase
+                               kernels; WCSP_HALO_PEER (1): SURVEY §8(f) f2 — one persistent
+                               cooperative kernel per device in which water crossing a slab
+                               boundary is a system-scope atomicMax into the neighbour's state
+                               word and the Step-4 test reads the neighbour's label
+                               in place (NVLink peer memory via CUDA IPC across GPUs; with
+                               nranks > 1 every rank's GPU must have peer access to its
+                               neighbours').  Outputs and work counters equal the single-device
+                               run's.  At most 8 virtual slabs. */
   int32_t nranks;           /* > 1: multi-GPU slab engine — this process owns slab `rank` of `nranks`
                                (one process per GPU); the slabs exchange boundary water and labels
                                with ncclSend/ncclRecv and combine the cycle decision with one

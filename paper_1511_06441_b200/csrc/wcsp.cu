@@ -99,6 +99,16 @@ struct wcsp_handle {
   long long f2stop = 0;
   long long* stair = nullptr;
   unsigned stair_cap = 0;
+  // peer halo: one cooperative kernel, boundary fused over peer memory
+  int halo = WCSP_HALO_COPY;
+  unsigned peer_per = 0;                             // blocks per slab in the peer kernel
+  unsigned long long* xbar = nullptr;                // [0] cross-slab barrier, [1] watchdog flag
+  unsigned long long* xbar_ptr = nullptr;            // multi-GPU: rank 0's counter, mapped
+  Ctl** d_pctl = nullptr;                            // multi-GPU: every rank's control block (mapped)
+  std::vector<void*> ipc_opened;                     // peer allocations mapped with CUDA IPC
+  unsigned long long* peer_sw[2] = {nullptr, nullptr};
+  unsigned* peer_tb[2] = {nullptr, nullptr};
+  unsigned peer_shift[2] = {0, 0}, peer_goff[2] = {0, 0};
 };
 
 namespace {
@@ -123,7 +133,8 @@ cudaError_t set_smem_attrs() {
   const int bytes = (int)sizeof(Smem);
   void* fns[] = {reinterpret_cast<void*>(&k_persistent<D>), reinterpret_cast<void*>(&k_sweep<D>),
                  reinterpret_cast<void*>(&k_treat<D>), reinterpret_cast<void*>(&k_wheel_persistent<D>),
-                 reinterpret_cast<void*>(&k_wheel_fire<D>), reinterpret_cast<void*>(&k_wheel_treat<D>)};
+                 reinterpret_cast<void*>(&k_wheel_fire<D>), reinterpret_cast<void*>(&k_wheel_treat<D>),
+                 reinterpret_cast<void*>(&k_wheel_peer<D>)};
   for (void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
@@ -316,6 +327,8 @@ void destroy_comm(void* comm);
 void release(wcsp_handle* h) {
   if (h->comm) destroy_comm(h->comm);
   h->comm = nullptr;
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  h->ipc_opened.clear();
   for (wcsp_handle* c : h->children) {
     release(c);
     delete c;
@@ -324,7 +337,7 @@ void release(wcsp_handle* h) {
   void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->tbits, h->barr,
                   h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
                   h->d_cnt, h->d_ghost, h->g_out_lo, h->g_out_hi, h->g_in_lo, h->g_in_hi, h->l_out_lo,
-                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair};
+                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -642,6 +655,7 @@ struct NcclApi {
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
@@ -661,10 +675,12 @@ NcclApi& nccl_api() {
   api.send = (decltype(api.send))dlsym(lib, "ncclSend");
   api.recv = (decltype(api.recv))dlsym(lib, "ncclRecv");
   api.allReduce = (decltype(api.allReduce))dlsym(lib, "ncclAllReduce");
+  api.allGather = (decltype(api.allGather))dlsym(lib, "ncclAllGather");
   api.groupStart = (decltype(api.groupStart))dlsym(lib, "ncclGroupStart");
   api.groupEnd = (decltype(api.groupEnd))dlsym(lib, "ncclGroupEnd");
   api.errStr = (decltype(api.errStr))dlsym(lib, "ncclGetErrorString");
   api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.send && api.recv && api.allReduce &&
+           api.allGather &&
            api.groupStart && api.groupEnd && api.errStr;
   return api;
 }
@@ -694,6 +710,9 @@ wcsp_status host_validate(const wcsp_problem* p, unsigned long long* nB, int* f1
   *f1max = fmax;
   return WCSP_REACHED;
 }
+
+void* peer_fn_d(int d);
+wcsp_status peer_connect(wcsp_handle* g);
 
 wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_handle** out) {
   if (p->mem != WCSP_MEM_HOST) return fail(WCSP_EINVAL, "the slab engine takes host arrays");
@@ -793,9 +812,28 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
     return bail(fail(WCSP_ENOMEM, "slab control array"));
   if (cudaMallocHost(&g->h_ctl, sizeof(Ctl)) != cudaSuccess) return bail(fail(WCSP_ENOMEM, "pinned control block"));
   g->grid = g->children[0]->grid;
+  if (opt.halo == WCSP_HALO_PEER) {
+    if (!dist && R > MAX_VSLABS) return bail(fail(WCSP_EINVAL, "at most %d virtual slabs with the peer halo", MAX_VSLABS));
+    int per_sm = 0, nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peer_fn_d(d), THREADS, sizeof(Smem)) != cudaSuccess ||
+        per_sm < 1)
+      return bail(fail(WCSP_ECUDA, "peer-halo kernel cannot be resident"));
+    const int per = std::min(g->grid, per_sm * nsm / (dist ? 1 : R));
+    if (per < 1) return bail(fail(WCSP_EINVAL, "too many slabs for one device"));
+    g->halo = WCSP_HALO_PEER;
+    g->peer_per = (unsigned)per;
+    if (cudaMalloc(&g->xbar, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(g->xbar, 0, 4 * sizeof(unsigned long long)) != cudaSuccess)
+      return bail(fail(WCSP_ENOMEM, "peer barrier"));
+    if (dist && (st = peer_connect(g)) != WCSP_REACHED) return bail(st);
+  }
   *out = g;
   return WCSP_REACHED;
 }
+
+wcsp_status group_collect(wcsp_handle* g, wcsp_result* r, int* status);
+wcsp_status dist_collect(wcsp_handle* g, wcsp_result* r, int* status);
 
 template <int D>
 void group_cycle(wcsp_handle* g, const std::vector<Dev>& devs) {
@@ -873,6 +911,13 @@ wcsp_status group_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
     if (s0 != ST_RUNNING) break;
     batch = std::min(batch * 2, 64);
   }
+  return group_collect(g, r, status);
+}
+
+// Results of a virtual slab group: counters summed over the slabs, Y = min over the slabs.
+wcsp_status group_collect(wcsp_handle* g, wcsp_result* r, int* status) {
+  auto& ch = g->children;
+  const int R = (int)ch.size();
   CK(cudaEventRecord(g->e1, g->stream));
   std::vector<Ctl> cs(R);
   for (int i = 0; i < R; ++i) CK(cudaMemcpyAsync(&cs[i], ch[i]->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
@@ -1004,8 +1049,16 @@ wcsp_status dist_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
     if (s0 != ST_RUNNING) break;
     batch = std::min(batch * 2, 64);
   }
+  return dist_collect(g, r, status);
+}
+
+// Results of the multi-GPU slab engine: totals over the ranks — counters (sum), Y (min),
+// overflow need (max) — with three small allreduces.
+wcsp_status dist_collect(wcsp_handle* g, wcsp_result* r, int* status) {
+  NcclApi& nc = nccl_api();
+  wcsp_handle* c = g->children[0];
+  ncclComm_t comm = (ncclComm_t)g->comm;
   CK(cudaEventRecord(g->e1, g->stream));
-  // totals over the ranks: counters (sum), Y (min), overflow need (max)
   Ctl cs;
   CK(cudaMemcpyAsync(&cs, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
@@ -1054,11 +1107,157 @@ wcsp_status dist_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
   return WCSP_REACHED;
 }
 
+// ---------------------------------------------------------------------------
+// Peer halo (k_wheel_peer in wcsp_wheel.cuh).
+// ---------------------------------------------------------------------------
+Dev make_peer_dev(wcsp_handle* g, int i) {
+  wcsp_handle* c = g->children[i];
+  Dev s = make_dev(c);
+  const bool dist = g->comm != nullptr;
+  s.peer = 1;
+  s.slab = 1;
+  s.nblocks = g->peer_per;
+  s.blk0 = dist ? 0u : (unsigned)i * g->peer_per;
+  s.plo_end = c->glo ? c->plane : 0u;
+  if (dist) {
+    for (int k = 0; k < 2; ++k) {
+      s.psw[k] = g->peer_sw[k]; s.ptb[k] = g->peer_tb[k];
+      s.pshift[k] = g->peer_shift[k]; s.pgoff[k] = g->peer_goff[k];
+    }
+    s.pctl = g->d_pctl;
+    s.nslab = g->nranks;
+    s.islab = g->rank;
+  } else {
+    if (c->glo) {                  // our lower ghost plane = the lower slab's last owned plane
+      wcsp_handle* lo = g->children[i - 1];
+      s.psw[0] = lo->sw; s.ptb[0] = lo->tbits;
+      s.pshift[0] = (unsigned)(lo->N - 2ull * c->plane); s.pgoff[0] = lo->goff;
+    }
+    if (c->ghi) {                  // our upper ghost plane = the upper slab's first owned plane
+      wcsp_handle* hi = g->children[i + 1];
+      s.psw[1] = hi->sw; s.ptb[1] = hi->tbits;
+      s.pshift[1] = c->plane - c->ghost_hi_start; s.pgoff[1] = hi->goff;
+    }
+    s.pctl = g->d_ctls;
+    s.nslab = (int)g->children.size();
+    s.islab = i;
+  }
+  unsigned long long* xb = g->xbar_ptr ? g->xbar_ptr : g->xbar;
+  s.xbar = xb;
+  s.xabort = reinterpret_cast<unsigned*>(xb + 1);
+  return s;
+}
+
+void* peer_fn_d(int d) {
+  return d == 1 ? reinterpret_cast<void*>(&k_wheel_peer<1>) : d == 2 ? reinterpret_cast<void*>(&k_wheel_peer<2>)
+       : d == 3 ? reinterpret_cast<void*>(&k_wheel_peer<3>) : reinterpret_cast<void*>(&k_wheel_peer<4>);
+}
+
+wcsp_status peer_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
+  wcsp_status st;
+  auto& ch = g->children;
+  const int n = (int)ch.size();
+  const bool dist = g->comm != nullptr;
+  g->launches = 0;
+  CK(cudaEventRecord(g->e0, g->stream));
+  for (auto* c : ch) {
+    c->M = g->M;
+    if ((st = reset_ctl(c)) != WCSP_REACHED) return st;
+    if ((st = launch_init(c)) != WCSP_REACHED) return st;
+    g->launches += 1;
+  }
+  if (!dist || g->rank == 0) CK(cudaMemsetAsync(g->xbar, 0, 4 * sizeof(unsigned long long), g->stream));
+  if (dist) {                      // every rank has reset its state before any rank's kernel starts
+    NcclApi& nc = nccl_api();
+    NCK(nc.allReduce(g->xbar + 2, g->xbar + 3, 1, ncclUint64, ncclMax, (ncclComm_t)g->comm, g->stream));
+  }
+  CK(cudaEventRecord(g->em, g->stream));
+  DevSet set{};
+  set.per = g->peer_per;
+  set.n = n;
+  for (int i = 0; i < n; ++i) set.d[i] = make_peer_dev(g, i);
+  void* args[] = {&set};
+  CK(cudaLaunchCooperativeKernel(peer_fn_d(g->d), dim3(n * g->peer_per), dim3(THREADS), args, sizeof(Smem),
+                                 g->stream));
+  g->launches += 1;
+  return dist ? dist_collect(g, r, status) : group_collect(g, r, status);
+}
+
+// Multi-GPU peer halo: map the neighbours' state words and bitmaps, every rank's
+// control block and rank 0's barrier counter with CUDA IPC (handles all-gathered
+// over NCCL).
+struct PeerBlob {
+  cudaIpcMemHandle_t sw, tb, ctl, xbar;
+  unsigned long long nloc, goff;
+};
+
+wcsp_status peer_connect(wcsp_handle* g) {
+  NcclApi& nc = nccl_api();
+  wcsp_handle* c = g->children[0];
+  const int R = g->nranks, me = g->rank;
+  PeerBlob mine{};
+  CK(cudaIpcGetMemHandle(&mine.sw, c->sw));
+  CK(cudaIpcGetMemHandle(&mine.tb, c->tbits));
+  CK(cudaIpcGetMemHandle(&mine.ctl, c->ctl));
+  CK(cudaIpcGetMemHandle(&mine.xbar, g->xbar));
+  mine.nloc = c->N;
+  mine.goff = c->goff;
+  uint8_t* dbuf = nullptr;
+  CK(cudaMalloc(&dbuf, (size_t)(R + 1) * sizeof(PeerBlob)));
+  CK(cudaMemcpy(dbuf + (size_t)R * sizeof(PeerBlob), &mine, sizeof(PeerBlob), cudaMemcpyHostToDevice));
+  std::vector<PeerBlob> all(R);
+  const ncclResult_t nr = nc.allGather(dbuf + (size_t)R * sizeof(PeerBlob), dbuf, sizeof(PeerBlob), ncclUint8,
+                                       (ncclComm_t)g->comm, g->stream);
+  if (nr != ncclSuccess) { cudaFree(dbuf); return fail(WCSP_ENCCL, "ncclAllGather: %s", nc.errStr(nr)); }
+  cudaError_t e = cudaMemcpyAsync(all.data(), dbuf, (size_t)R * sizeof(PeerBlob), cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(dbuf);
+  if (e != cudaSuccess) return fail(WCSP_ECUDA, "peer handle exchange: %s", cudaGetErrorString(e));
+  auto open = [&](const cudaIpcMemHandle_t& hd, void** p) -> wcsp_status {
+    const cudaError_t oe = cudaIpcOpenMemHandle(p, hd, cudaIpcMemLazyEnablePeerAccess);
+    if (oe != cudaSuccess)
+      return fail(WCSP_ECUDA, "cudaIpcOpenMemHandle: %s (peer access between the GPUs required)",
+                  cudaGetErrorString(oe));
+    g->ipc_opened.push_back(*p);
+    return WCSP_REACHED;
+  };
+  wcsp_status st;
+  std::vector<Ctl*> ctls(R, nullptr);
+  for (int r = 0; r < R; ++r) {
+    if (r == me) { ctls[r] = c->ctl; continue; }
+    void* p = nullptr;
+    if ((st = open(all[r].ctl, &p)) != WCSP_REACHED) return st;
+    ctls[r] = (Ctl*)p;
+  }
+  if (me > 0) {
+    void *sw = nullptr, *tb = nullptr, *xb = nullptr;
+    if ((st = open(all[me - 1].sw, &sw)) != WCSP_REACHED) return st;
+    if ((st = open(all[me - 1].tb, &tb)) != WCSP_REACHED) return st;
+    if ((st = open(all[0].xbar, &xb)) != WCSP_REACHED) return st;
+    g->peer_sw[0] = (unsigned long long*)sw; g->peer_tb[0] = (unsigned*)tb;
+    g->peer_shift[0] = (unsigned)(all[me - 1].nloc - 2ull * c->plane);
+    g->peer_goff[0] = (unsigned)all[me - 1].goff;
+    g->xbar_ptr = (unsigned long long*)xb;
+  }
+  if (me < R - 1) {
+    void *sw = nullptr, *tb = nullptr;
+    if ((st = open(all[me + 1].sw, &sw)) != WCSP_REACHED) return st;
+    if ((st = open(all[me + 1].tb, &tb)) != WCSP_REACHED) return st;
+    g->peer_sw[1] = (unsigned long long*)sw; g->peer_tb[1] = (unsigned*)tb;
+    g->peer_shift[1] = c->plane - c->ghost_hi_start;
+    g->peer_goff[1] = (unsigned)all[me + 1].goff;
+  }
+  CK(cudaMalloc(&g->d_pctl, R * sizeof(Ctl*)));
+  CK(cudaMemcpy(g->d_pctl, ctls.data(), R * sizeof(Ctl*), cudaMemcpyHostToDevice));
+  return WCSP_REACHED;
+}
+
 wcsp_status group_solve(wcsp_handle* g, wcsp_result* out) {
   wcsp_result r;
   int status = ST_RUNNING;
   for (int attempt = 0; attempt < 6; ++attempt) {
-    wcsp_status st = g->comm ? dist_solve_once(g, &r, &status) : group_solve_once(g, &r, &status);
+    wcsp_status st = g->halo == WCSP_HALO_PEER ? peer_solve_once(g, &r, &status)
+                   : g->comm ? dist_solve_once(g, &r, &status) : group_solve_once(g, &r, &status);
     if (st != WCSP_REACHED) return st;
     if (status != WCSP_EOVERFLOW) break;
     for (auto* c : g->children) {     // grow every child's wheel storage and re-run
@@ -1100,6 +1299,7 @@ wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handl
   if (opt.engine < WCSP_ENGINE_PERSISTENT || opt.engine > WCSP_ENGINE_WHEEL_STEPPED)
     return fail(WCSP_EINVAL, "bad engine %d", opt.engine);
   if (opt.trace_cap < 0 || opt.cycle_budget < 0 || opt.phantom_capacity < 0) return fail(WCSP_EINVAL, "negative option");
+  if (opt.halo != WCSP_HALO_COPY && opt.halo != WCSP_HALO_PEER) return fail(WCSP_EINVAL, "bad halo %d", opt.halo);
 
   if (opt.slabs > 1 || opt.nranks > 1 || opt.nccl_id) return create_group(p, opt, out);
   return create_impl(p, opt, nullptr, out);

@@ -86,6 +86,7 @@ struct Ctl {
   View view;
   Acc acc[3];
   unsigned long long bar;          // grid barrier arrivals (persistent engines)
+  unsigned long long rel;          // peer halo: epoch released by this slab's leader block
   unsigned abort, n_barr;          // barrier watchdog fired; B-arrival list length
   long long F1, F2, X, Y;
   long long via;
@@ -146,6 +147,19 @@ struct Dev {
   unsigned long long* ghost_out_lo;   // water handed to the lower neighbour's boundary plane
   unsigned long long* ghost_out_hi;   // ... to the upper neighbour's
   int slab;                        // 1: decide uses the reduced global proposal (ctl->gprop)
+  unsigned blk0;                   // first block of this slab in the launch (peer halo: slab * nblocks)
+  // peer halo: a ghost index resolves to the neighbouring slab's own memory
+  // (the same device for virtual slabs, NVLink peer memory mapped with CUDA IPC across GPUs)
+  int peer;
+  unsigned plo_end;                // local indices < plo_end are the lower ghost plane
+  unsigned long long* psw[2];      // lower / upper neighbour's state words
+  unsigned* ptb[2];                // lower / upper neighbour's triggered bitmaps
+  unsigned pshift[2];              // ghost index + pshift = the neighbour's local index (mod 2^32)
+  unsigned pgoff[2];               // the neighbour's global offset
+  Ctl* const* pctl;                // every slab's control block (proposals, target hits)
+  int nslab, islab;
+  unsigned long long* xbar;        // cross-slab barrier arrivals (monotone)
+  unsigned* xabort;                // cross-slab watchdog flag
   // staircase mode (wcsp_staircase): record every strictly better target arrival, keep going
   int staircase;
   long long f2stop;
@@ -404,27 +418,64 @@ __device__ __forceinline__ void block_reduce_commit(Smem& sm, unsigned dmin, uns
 // flight before it needs their results: arrive_atomic issues the atomicMax,
 // arrive_post acts on its return value (the bitmap OR is a fire-and-forget
 // reduction).
+// Peer halo: where local index D lives (its owner's state words and bitmap, the index
+// there, the owner's global offset).  Without PEER every index is local.
+struct Loc { unsigned long long* sw; unsigned* tb; unsigned idx; unsigned goff; };
+template <bool PEER>
+__device__ __forceinline__ Loc locate(const Dev& s, unsigned D) {
+  if constexpr (PEER) {
+    if (D < s.plo_end) return Loc{s.psw[0], s.ptb[0], D + s.pshift[0], s.pgoff[0]};
+    if (D >= s.ghost_hi_start) return Loc{s.psw[1], s.ptb[1], D + s.pshift[1], s.pgoff[1]};
+  }
+  return Loc{s.sw, s.tbits, D, s.goff};
+}
+
+// Every state-word atomic of the peer halo is system-scoped: the neighbour GPU's
+// threads update the same words.
+__device__ __forceinline__ unsigned atom_max_sys(unsigned* a, unsigned v) {
+  unsigned old;
+  asm volatile("atom.relaxed.sys.global.max.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void atom_or_sys(unsigned* a, unsigned v) {
+  asm volatile("red.relaxed.sys.global.or.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+template <bool PEER = false>
 __device__ __forceinline__ unsigned arrive_atomic(const Dev& s, const View& v, bool go, unsigned D, int cand) {
-  return go ? atom_max_hint(tmp_ptr(s.sw, D), (v.stamp << 16) | (unsigned)cand, pol_last()) : (v.stamp << 16);
+  if constexpr (PEER) {
+    if (!go) return v.stamp << 16;
+    const Loc L = locate<true>(s, D);
+    return atom_max_sys(tmp_ptr(L.sw, L.idx), (v.stamp << 16) | (unsigned)cand);
+  } else {
+    return go ? atom_max_hint(tmp_ptr(s.sw, D), (v.stamp << 16) | (unsigned)cand, pol_last()) : (v.stamp << 16);
+  }
 }
 
 // src is a GLOBAL vertex index (local index + s.goff); D is local.
+template <bool PEER = false>
 __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* acc, unsigned old, unsigned D,
                                             int cand, unsigned src, unsigned via) {
   const unsigned os = old >> 16;
   if (os == 0xFFFFu) {
     if (old == TMP_B) {            // termination 1°: a vertex of B is reached
-      const unsigned Dg = D + s.goff;
+      const Loc L = locate<PEER>(s, D);
+      const unsigned Dg = L.idx + L.goff;
       atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - Dg));
       const unsigned k = atomicAdd(&s.ctl->n_barr, 1u);
       if (k < s.barr_cap) s.barr[k] = BArr{Dg, (unsigned)cand, src, via};
-    } else if (old >= TMP_GHOST) { // D belongs to a neighbouring slab: hand the water to its owner
+    } else if (!PEER && old >= TMP_GHOST) {   // D belongs to a neighbouring slab: hand the water to its owner
       unsigned long long* slot = D < s.plane ? s.ghost_out_lo + D : s.ghost_out_hi + (D - s.ghost_hi_start);
       atomicMax(slot, ((unsigned long long)v.stamp << 48) | ((unsigned long long)(unsigned)cand << 32) |
                           ((unsigned long long)(0x7FFFFFFFu - src) << 1) | (unsigned long long)(via ? 0u : 1u));
     }
   } else if (os != v.stamp) {      // first arrival of the cycle: D is triggered (dedupe)
-    atomicOr(s.tbits + (D >> 5), 1u << (D & 31u));
+    if constexpr (PEER) {
+      const Loc L = locate<true>(s, D);
+      atom_or_sys(L.tb + (L.idx >> 5), 1u << (L.idx & 31u));
+    } else {
+      atomicOr(s.tbits + (D >> 5), 1u << (D & 31u));
+    }
   }
 }
 
@@ -569,7 +620,7 @@ __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsi
 // WHEEL = false: lanes are residual bytes in res[q]; phantoms go to the pool.
 // WHEEL = true : lanes and phantoms are events filed at t + f1 (wcsp_wheel.cuh).
 // ---------------------------------------------------------------------------
-template <int D, bool WHEEL_ENGINE>
+template <int D, bool WHEEL_ENGINE, bool PEER = false>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
                                           unsigned& dmin, unsigned long long& created,
                                           unsigned long long& relabels, unsigned long long& triggered,
@@ -590,7 +641,7 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long long rec, unsigned delay, long long t);
 __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t);
 
-template <int D, bool WHEEL_ENGINE>
+template <int D, bool WHEEL_ENGINE, bool PEER>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
                                           unsigned& dmin, unsigned long long& created,
                                           unsigned long long& relabels, unsigned long long& triggered,
@@ -617,7 +668,12 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     const bool test = trig && f1j != 0 && lstar - (int)f2j > 0;
     // L1-cached read: this phase never writes the temp half, the label half only moves to
     // max(L, temp) (benign), and the grid barrier before the phase invalidated L1
-    swr[j] = test ? s.sw[q + s.off[j]] : 0xFFFFull;   // untested lanes read as "removed"
+    if constexpr (PEER) {            // a neighbour in the next slab is read in its owner's memory
+      const Loc L = locate<true>(s, q + s.off[j]);
+      swr[j] = test ? (L.sw == s.sw ? s.sw[L.idx] : __ldcv(L.sw + L.idx)) : 0xFFFFull;
+    } else {
+      swr[j] = test ? s.sw[q + s.off[j]] : 0xFFFFull;   // untested lanes read as "removed"
+    }
   }
   LW neww = 0;
   unsigned fmax = 0, pm = 0;
@@ -695,15 +751,15 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
 // Flush hook of the wheel (defined in wcsp_wheel.cuh).
 __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, bool final_flush);
 
-template <int D, bool WHEEL_ENGINE>
+template <int D, bool WHEEL_ENGINE, bool PEER = false>
 __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   Acc* acc = &s.ctl->acc[v.c % 3];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const unsigned nwin = (s.nwords + WIN_WORDS - 1) / WIN_WORDS;
   // every block owns one contiguous slab of windows: its phantoms / events come from a
   // compact region of the grid, so a run's destinations share sectors and L2 lines
-  const unsigned rounds = (nwin + gridDim.x * WARPS - 1) / (gridDim.x * WARPS);
-  const unsigned win0 = blockIdx.x * rounds * WARPS;
+  const unsigned rounds = (nwin + s.nblocks * WARPS - 1) / (s.nblocks * WARPS);
+  const unsigned win0 = (blockIdx.x - s.blk0) * rounds * WARPS;
   unsigned dmin = 0xFFFFFFFFu;
   unsigned long long created = 0, relabels = 0, triggered = 0, lanes_started = 0, tested = 0;
   if constexpr (WHEEL_ENGINE) {
@@ -715,7 +771,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
       const unsigned q = b + lane < total ? sm.wl[warp][b + lane] : 0xFFFFFFFFu;
-      treat_one<D, WHEEL_ENGINE>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
+      treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
     }
     if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, false);
     else qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);

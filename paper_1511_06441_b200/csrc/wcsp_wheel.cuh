@@ -36,7 +36,7 @@ constexpr int FIRE_ITEMS = 8;             // events per lane per fire chunk (ato
 // walk compact regions of the state array (L2-resident) instead of the
 // whole front at once.
 __device__ __forceinline__ void file_run(const Dev& s, unsigned b, unsigned long long pos, unsigned cnt) {
-  const size_t slot = (size_t)b * s.nblocks + blockIdx.x;
+  const size_t slot = (size_t)b * s.nblocks + (blockIdx.x - s.blk0);
   const unsigned k = atomicAdd(s.bndesc + slot, 1u);
   if (k < s.dcap) s.bdesc[slot * s.dcap + k] = (pos << 24) | cnt;
   else atomicOr(&s.ctl->wheel_overflow, 2u);
@@ -155,12 +155,13 @@ __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
 // fires the runs its own slab filed; the runs are cut into chunks of
 // FIRE_ITEMS * 32 events that the block's warps take in turn (a prefix sum of
 // chunk counts over the block's runs lives in shared memory).
-template <int D>
+template <int D, bool PEER = false>
 __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   Acc* acc = &s.ctl->acc[v.c % 3];
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
-  if (threadIdx.x == 0) s.bndesc[(size_t)((v.t - v.delta) & (WHEEL - 1)) * s.nblocks + blockIdx.x] = 0;
-  const size_t slot = (size_t)b * s.nblocks + blockIdx.x;
+  const unsigned vb = blockIdx.x - s.blk0;
+  if (threadIdx.x == 0) s.bndesc[(size_t)((v.t - v.delta) & (WHEEL - 1)) * s.nblocks + vb] = 0;
+  const size_t slot = (size_t)b * s.nblocks + vb;
   const unsigned nd = min(__ldcg(s.bndesc + slot), s.dcap);
   const unsigned long long* dl = s.bdesc + slot * s.dcap;
   constexpr unsigned CH = FIRE_ITEMS * 32;
@@ -216,14 +217,15 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         arr += valid;
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
-        old[it] = arrive_atomic(s, v, valid, src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));
+        old[it] = arrive_atomic<PEER>(s, v, valid, src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));
       }
 #pragma unroll
       for (int it = 0; it < FIRE_ITEMS; ++it) {
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
         const unsigned via = ((e[it] >> EV_LANE_BIT) & 1) ? 0u : 1u;
-        arrive_post(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu), src + s.goff, via);
+        arrive_post<PEER>(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu), src + s.goff,
+                          via);
       }
     }
   }
@@ -269,7 +271,7 @@ __device__ Prop wheel_propose(const Dev& s, const View& v, long long* need) {
 // decide for the wheel (Step 6 + time skipping).  Single device: g = its own
 // proposal; slab engine: g = the max-combined proposals of all slabs.  Reads
 // only state no block writes during decide.
-__device__ void wheel_decide(const Dev& s, View& v, bool writer) {
+__device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gext = nullptr) {
   Acc* a = &s.ctl->acc[v.c % 3];
   Ctl* C = s.ctl;
   View nv = v;
@@ -284,7 +286,9 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer) {
   long long need = 0;
   const Prop L = wheel_propose(s, v, &need);
   Prop G = L;
-  if (s.slab) {
+  if (gext) {
+    G = *gext;
+  } else if (s.slab) {
     const volatile Prop* gp = &C->gprop;
     G.bhit = gp->bhit; G.negk = gp->negk; G.pending = gp->pending; G.overflow = gp->overflow;
   }
@@ -422,8 +426,8 @@ __global__ void __launch_bounds__(THREADS) k_slab_scatter_labels(Dev s, const un
 // Maintenance (rare): forget stale temps and refresh lane-expiry times so the
 // 16-bit stamp and texp comparisons stay unambiguous.
 __device__ __forceinline__ void wheel_maintain(const Dev& s, long long t) {
-  for (unsigned long long i = (unsigned long long)blockIdx.x * THREADS + threadIdx.x; i < s.N;
-       i += (unsigned long long)gridDim.x * THREADS) {
+  for (unsigned long long i = (unsigned long long)(blockIdx.x - s.blk0) * THREADS + threadIdx.x; i < s.N;
+       i += (unsigned long long)s.nblocks * THREADS) {
     unsigned* tp = tmp_ptr(s.sw, (unsigned)i);
     if ((*tp >> 16) != 0xFFFFu) *tp = 0u;
     unsigned* lp = lbl_ptr(s.sw, (unsigned)i);
@@ -517,6 +521,144 @@ __global__ void k_wheel_decide(Dev s) {
 __global__ void __launch_bounds__(THREADS) k_wheel_maintain(Dev s) {
   const long long t = ((volatile View*)&s.ctl->view)->t;
   wheel_maintain(s, t);
+}
+
+// ---------------------------------------------------------------------------
+// Peer halo: every slab runs the persistent wheel cycle in
+// ONE cooperative kernel per device, and the halo is fused into it — water
+// that crosses a slab boundary is a system-scope atomicMax straight into the
+// neighbour's state word (plus its bitmap bit), and the Step-4 neighbour test
+// reads the neighbour's current label in its own memory.  No ghost copies, no
+// host round trip, no stale labels: outputs AND work counters equal the
+// single-device run.  Across GPUs the neighbour's arrays are NVLink peer
+// memory (CUDA IPC); on one device (virtual slabs) they are the other slabs'
+// allocations and the slabs are groups of blocks of the same launch.
+//
+// Barrier: the blocks of a slab meet on its control block (ctl->bar); the
+// slab's leader block then meets the other leaders on the cross-slab counter
+// (system scope) and releases its slab with ctl->rel = epoch.
+// ---------------------------------------------------------------------------
+constexpr int MAX_VSLABS = 8;
+struct DevSet { Dev d[MAX_VSLABS]; unsigned per; int n; };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_add_release_sys(unsigned long long* p, unsigned long long x) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long x) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+
+__device__ __forceinline__ bool peer_sync(const Dev& s, Smem& sm, unsigned long long epoch,
+                                          unsigned long long* fin = nullptr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (fin) {
+      const unsigned long long busy = globaltimer_ns() - sm.tphase;
+      atomicMax(fin, busy);
+      atomicAdd(fin + 1, busy);
+    }
+    __threadfence_system();        // this block's writes, remote atomics included, before arriving
+    atomicAdd(&s.ctl->bar, 1ull);
+    const unsigned long long t0 = globaltimer_ns();
+    unsigned ok = 1;
+    auto timed_out = [&]() {
+      if (*(volatile unsigned*)&s.ctl->abort || *(volatile unsigned*)s.xabort) return true;
+      if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) {
+        atomicExch(&s.ctl->abort, 1u);
+        atomicExch(s.xabort, 1u);
+        return true;
+      }
+      return false;
+    };
+    if (blockIdx.x == s.blk0) {    // leader: all blocks of the slab, then all slabs
+      while (ld_acquire(&s.ctl->bar) < epoch * s.nblocks) {
+        __nanosleep(32);
+        if (timed_out()) { ok = 0; break; }
+      }
+      if (ok) {
+        __threadfence_system();
+        red_add_release_sys(s.xbar, 1ull);
+        while (ld_acquire_sys(s.xbar) < epoch * (unsigned long long)s.nslab) {
+          __nanosleep(64);
+          if (timed_out()) { ok = 0; break; }
+        }
+      }
+      if (ok) st_release_gpu(&s.ctl->rel, epoch);
+    } else {
+      while (ld_acquire(&s.ctl->rel) < epoch) {
+        __nanosleep(32);
+        if (timed_out()) { ok = 0; break; }
+      }
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    sm.flag = ok;
+  }
+  __syncthreads();
+  const bool ok = sm.flag != 0;
+  __syncthreads();
+  return ok;
+}
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 4) k_wheel_peer(const __grid_constant__ DevSet set) {
+  const Dev& s = set.d[blockIdx.x / set.per];
+  Smem& sm = smem();
+  init_smem(sm);
+  View v;
+  load_view(s, sm, v);
+  const bool leader = blockIdx.x == s.blk0;
+  unsigned long long epoch = 0;
+  while (v.status == ST_RUNNING) {
+    if (v.c > 0) {
+      if (leader && threadIdx.x == 0) wheel_cycle_start(s, v);
+      if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
+      wheel_fire<D, true>(s, v, sm);
+      if (!peer_sync(s, sm, ++epoch, &s.ctl->fin[v.c & 1][0][0])) return;
+    }
+    if (leader && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
+    if (threadIdx.x == 0) {          // a target reached in any slab ends the run (1°)
+      unsigned long long bh = 0;
+      for (int i = 0; i < s.nslab; ++i) bh = max(bh, __ldcv(&s.pctl[i]->acc[v.c % 3].bhit));
+      sm.bhit = bh;
+    }
+    __syncthreads();
+    const unsigned long long bhit = sm.bhit;
+    __syncthreads();
+    if (!bhit) {
+      if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
+      phase_treat<D, true, true>(s, v, sm);
+      if (!peer_sync(s, sm, ++epoch, &s.ctl->fin[v.c & 1][1][0])) return;
+    }
+    if (leader && threadIdx.x == 0) {   // this slab's proposal for the decision
+      long long need = 0;
+      s.ctl->prop = wheel_propose(s, v, &need);
+    }
+    if (!peer_sync(s, sm, ++epoch)) return;
+    const View prev = v;
+    if (threadIdx.x == 0) {          // every slab takes the same decision from the combined proposal
+      Prop G{0, -(long long)WHEEL, 0, 0};
+      for (int i = 0; i < s.nslab; ++i) {
+        const volatile Prop* p = &s.pctl[i]->prop;
+        G.bhit = max(G.bhit, (long long)p->bhit); G.negk = max(G.negk, (long long)p->negk);
+        G.pending = max(G.pending, (long long)p->pending); G.overflow = max(G.overflow, (long long)p->overflow);
+      }
+      View nv = v;
+      wheel_decide(s, nv, leader, &G);
+      sm.view = nv;
+    }
+    __syncthreads();
+    v = sm.view;
+    __syncthreads();
+    if (needs_maint(prev, v)) {
+      wheel_maintain(s, v.t);
+      if (!peer_sync(s, sm, ++epoch)) return;
+    }
+  }
 }
 
 }  // namespace wcspk

@@ -26,6 +26,8 @@ MEM_HOST, MEM_DEVICE = 0, 1
 JUMP, UNIT = 0, 1
 PERSISTENT, STEPPED, WHEEL, WHEEL_STEPPED = 0, 1, 2, 3
 ENGINES = {"persistent": PERSISTENT, "stepped": STEPPED, "wheel": WHEEL, "wheel_stepped": WHEEL_STEPPED}
+HALO_COPY, HALO_PEER = 0, 1
+HALOS = {"copy": HALO_COPY, "peer": HALO_PEER}
 _STATUS = {0: "REACHED", 1: "INFEASIBLE", 2: "EINVAL", 3: "EMISMATCH", 4: "EBUDGET", 5: "ENOMEM",
            6: "ECUDA", 7: "ENCCL", 8: "EOVERFLOW"}
 
@@ -47,7 +49,7 @@ class _Options(ctypes.Structure):
     _fields_ = [("time_mode", ctypes.c_int32), ("engine", ctypes.c_int32), ("demote_twin", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("cycle_budget", ctypes.c_int64),
                 ("phantom_capacity", ctypes.c_int64), ("trace_cap", ctypes.c_int64),
-                ("stream", ctypes.c_void_p), ("slabs", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("stream", ctypes.c_void_p), ("slabs", ctypes.c_int32), ("halo", ctypes.c_int32),
                 ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
 
 
@@ -193,7 +195,7 @@ class Solver:
     def __init__(self, inst=None, *, shape=None, f1=None, f2=None, maskA=None, maskB=None, present=None,
                  M=None, time_mode: str = "jump", engine: str = "persistent", trace_cap: int = 0,
                  phantom_capacity: int = 0, cycle_budget: int = 0, device: int = 0, stream=None,
-                 slabs: int = 0, nranks: int = 1, rank: int = 0, nccl_id: bytes = None):
+                 slabs: int = 0, halo: str = "copy", nranks: int = 1, rank: int = 0, nccl_id: bytes = None):
         lib = load_library()
         self._lib = lib
         self._h = ctypes.c_void_p()
@@ -212,6 +214,7 @@ class Solver:
         o.trace_cap = int(trace_cap)
         o.stream = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         o.slabs = int(slabs)
+        o.halo = HALOS[halo]
         o.nranks = int(nranks)
         o.rank = int(rank)
         self._nccl_id = None

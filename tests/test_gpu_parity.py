@@ -360,3 +360,73 @@ def test_staircase_every_budget_in_one_run(engine):
             assert o.key() == want, (inst.shape, M, steps, o)
             checked += 1
     assert checked > 300
+
+
+@pytest.mark.parametrize("slabs", [2, 3, 5, 8])
+def test_slab_engine_peer_halo(slabs):
+    """the slab boundary fused into one persistent kernel over
+    peer memory (water crossing a boundary is a system-scope atomicMax into the
+    neighbour's state word; the Step-4 test reads the neighbour's label in
+    place).  No stale ghost labels, so outputs AND every work counter equal the
+    single-device run (and tier 5)."""
+    rng = np.random.default_rng(900 + slabs)
+    shapes = [(12, 12), (9, 20), (6, 6, 6), (5, 4, 11), (3, 3, 3, 8), (40,), (16, 16, 16)]
+    for i in range(50):
+        inst = I.random_small(rng, shapes=shapes, M_range=(5, 120), max_sources=4, max_targets=4,
+                              hole_prob=0.1 if i % 3 == 0 else 0.0)
+        if i % 7 == 3:
+            inst = inst.with_M(I.M_INF)
+        if i % 5 == 4:
+            inst = inst.with_sets(present=(rng.random(inst.N) > 0.1).astype(np.uint8))
+            if not (inst.maskA & inst.present).any() or not (inst.maskB & inst.present).any():
+                continue
+        if inst.shape[-1] < slabs:
+            continue
+        r1 = wcsp.solve(inst, engine="wheel")
+        rp = wcsp.solve(inst, engine="wheel", slabs=slabs, halo="peer")
+        assert rp.key() == r1.key() == oracle.solve_pruned(inst).key(), (inst.shape, inst.M, slabs, rp, r1)
+        assert model_counters(rp) == model_counters(r1), (inst.shape, inst.M, slabs, rp, r1)
+    for inst in (I.config_face((64, 64), 1, 300), I.config_face((32, 32, 32), 2, 200), I.fixture_D(),
+                 I.speedway_instance(20), I.config_face((48, 48, 48), 0, 260)):
+        if inst.shape[-1] < slabs:
+            continue
+        r1 = wcsp.solve(inst, engine="wheel")
+        rp = wcsp.solve(inst, engine="wheel", slabs=slabs, halo="peer")
+        assert rp.key() == r1.key() == oracle.solve_pruned(inst).key()
+        assert model_counters(rp) == model_counters(r1)
+
+
+def test_peer_halo_nccl_single_rank():
+    """The multi-GPU form of the peer halo (IPC handle exchange over NCCL, the
+    cross-rank barrier, per-rank result reduction) on one rank."""
+    for inst in (I.config_face((48, 48), 3, 220), I.config_face((16, 16, 16), 1, 120), I.fixture_B()):
+        r1 = wcsp.solve(inst, engine="wheel")
+        with wcsp.Solver(inst, engine="wheel", halo="peer", nranks=1, rank=0, nccl_id=wcsp.nccl_unique_id()) as s:
+            rn = s.solve()
+        assert rn.key() == r1.key()
+        assert model_counters(rn) == model_counters(r1)
+
+
+MODEL_GOLD = os.path.join(os.path.dirname(__file__), "golden", "model_counters.json")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key", ["C3s/0", "C2/0", "C3/0"])
+def test_full_size_counters_vs_model(key):
+    """BASELINE sizes: the metric's numerator (edge_updates) and every other
+    work counter equal oracle tier 5's (the paper's cycle run sequentially on
+    the CPU, stored by scripts/make_model_counters.py), for the default engine
+    and the sweep engine."""
+    gold = json.load(open(MODEL_GOLD))
+    if key not in gold:
+        pytest.skip(f"{key} not in {MODEL_GOLD}")
+    g = gold[key]
+    name, seed = key.split("/")
+    shape = {"C2": (1024, 1024), "C3": (256, 256, 256), "C3s": (128, 128, 128)}[name]
+    inst = I.config_face(shape, int(seed), I.M_INF).with_M(g["M"])
+    c = g["counters"]
+    want = (c["cycles"], c["work"], c["arrivals"], c["triggered"], c["created"], c["started"], c["relabels"])
+    for engine in ("wheel", "persistent"):
+        r = wcsp.solve(inst, engine=engine)
+        assert list(r.key()) == g["key"]
+        assert model_counters(r) == want, (key, engine, r)

@@ -70,6 +70,8 @@ struct wcsp_handle {
   unsigned long long* ev = nullptr;                  // wheel engines only
   unsigned long long ev_cap = 0;
   unsigned long long* bdesc = nullptr;
+  unsigned long long* spill = nullptr;               // [grid][spill_cap] staging overflow of the treat
+  unsigned spill_cap = 0;
   unsigned* bcounts = nullptr;                       // bnev [256] | bnlane [256] | bndesc [256][grid]
   unsigned dcap = 0;
   int f1max = 255;
@@ -142,6 +144,17 @@ cudaError_t set_smem_attrs() {
   return cudaSuccess;
 }
 
+// Treat window size (bitmap words per warp window).  Blocks own contiguous ranges of windows,
+// so a round count just above an integer leaves most warps idle in the last round: take 16
+// words when that gives at most one round or at least four (C2, C3), else 8 (C3s, P6 cubes).
+// WCSP_WIN_WORDS overrides (A/B runs).
+unsigned win_words_for(unsigned nwords, unsigned nblocks) {
+  if (const char* e = getenv("WCSP_WIN_WORDS")) return atoi(e) >= 16 ? 16u : 8u;
+  if (nblocks == 0) return 8u;
+  const double rounds16 = (double)nwords / (16.0 * nblocks * WARPS);
+  return rounds16 <= 1.0 || rounds16 >= 4.0 ? 16u : 8u;
+}
+
 Dev make_dev(const wcsp_handle* h) {
   Dev s{};
   s.N = (unsigned)h->N;
@@ -181,7 +194,10 @@ Dev make_dev(const wcsp_handle* h) {
   s.bndesc = h->bcounts ? h->bcounts + 2 * WHEEL : nullptr;
   s.dcap = h->dcap;
   s.f1max = h->f1max;
+  s.spill = h->spill;
+  s.spill_cap = h->spill_cap;
   s.nblocks = (unsigned)h->grid;
+  s.win_words = win_words_for(s.nwords, s.nblocks);
   s.goff = h->goff;
   s.plane = h->plane;
   s.ghost_hi_start = h->ghi ? h->ghost_hi_start : (unsigned)h->N;
@@ -337,7 +353,7 @@ void release(wcsp_handle* h) {
   void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->tbits, h->barr,
                   h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
                   h->d_cnt, h->d_ghost, h->g_out_lo, h->g_out_hi, h->g_in_lo, h->g_in_hi, h->l_out_lo,
-                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl};
+                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl, h->spill};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -581,6 +597,7 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
   int per_sm = 0;
   CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_fn_d(p->d, opt.engine), THREADS, sizeof(Smem)));
   if (per_sm < 1) CKH(fail(WCSP_ECUDA, "cycle kernel cannot be resident"));
+  if (const char* e = getenv("WCSP_BLOCKS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));   // A/B runs
   h->grid = per_sm * h->nsm;
   const size_t fb = (size_t)h->d * N;
   CKC(cudaMalloc(&h->d_f1, fb));
@@ -604,6 +621,11 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
     CKH(alloc_ring(h, std::max<unsigned long long>(opt.phantom_capacity > 0 ? cap : 2 * cap, (unsigned long long)h->grid * 2 * 4096)));
     CKH(alloc_desc(h, 32));
     CKC(cudaMalloc(&h->bcounts, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned)));
+    // spill room per block and flush period: a dense window round (e.g. the initial treatment
+    // of a whole boundary) can stage several times the shared-memory staging
+    h->spill_cap = (unsigned)std::min<unsigned long long>(16384, std::max<unsigned long long>(
+                                                                     2048, pow2_at_least(8 * N / h->grid)));
+    CKC(cudaMalloc(&h->spill, (size_t)h->grid * h->spill_cap * sizeof(unsigned long long)));
   } else {
     CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
     CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));
@@ -833,6 +855,15 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
 }
 
 wcsp_status group_collect(wcsp_handle* g, wcsp_result* r, int* status);
+
+// The ghost-plane exchange buffers carry cycle stamps, which restart at every solve (and every
+// overflow retry): clear them so no water of an earlier run is applied.
+wcsp_status clear_halo(wcsp_handle* c) {
+  const size_t pb = (size_t)c->plane;
+  for (unsigned long long* b : {c->g_out_lo, c->g_out_hi, c->g_in_lo, c->g_in_hi})
+    if (b) CK(cudaMemsetAsync(b, 0, pb * 8, c->stream));
+  return WCSP_REACHED;
+}
 wcsp_status dist_collect(wcsp_handle* g, wcsp_result* r, int* status);
 
 template <int D>
@@ -879,6 +910,7 @@ wcsp_status group_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
   for (auto* c : ch) {
     c->M = g->M;
     if ((st = reset_ctl(c)) != WCSP_REACHED) return st;
+    if ((st = clear_halo(c)) != WCSP_REACHED) return st;
     if ((st = launch_init(c)) != WCSP_REACHED) return st;
     g->launches += 1;
   }
@@ -1020,6 +1052,7 @@ wcsp_status dist_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
   CK(cudaEventRecord(g->e0, g->stream));
   c->M = g->M;
   if ((st = reset_ctl(c)) != WCSP_REACHED) return st;
+  if ((st = clear_halo(c)) != WCSP_REACHED) return st;
   if ((st = launch_init(c)) != WCSP_REACHED) return st;
   g->launches += 1;
   CK(cudaEventRecord(g->em, g->stream));
@@ -1117,6 +1150,7 @@ Dev make_peer_dev(wcsp_handle* g, int i) {
   s.peer = 1;
   s.slab = 1;
   s.nblocks = g->peer_per;
+  s.win_words = win_words_for(s.nwords, s.nblocks);
   s.blk0 = dist ? 0u : (unsigned)i * g->peer_per;
   s.plo_end = c->glo ? c->plane : 0u;
   if (dist) {

@@ -38,9 +38,15 @@ constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
 constexpr int SWEEP_ITEMS = 4;           // items per thread per chunk, sweep (unrolled for MLP)
 constexpr int CHUNK_MAX = THREADS * SWEEP_ITEMS;
-constexpr int QP_CAP = 3072;             // shared staging of phantoms / events (overflow -> direct append)
+#ifndef WCSP_MINB_SWEEP
+#define WCSP_MINB_SWEEP 4          // resident blocks per SM the sweep engine's kernels are compiled for
+#endif
+#ifndef WCSP_QP_CAP
+#define WCSP_QP_CAP 3072
+#endif
+constexpr int QP_CAP = WCSP_QP_CAP;             // shared staging of phantoms / events (overflow -> direct append)
 constexpr int QA_CAP = 2048;             // shared staging of active-list appends (never overflows)
-constexpr int WIN_WORDS = 8;             // triggered-bitmap words per warp window
+constexpr int WIN_WORDS = 16;            // max triggered-bitmap words per warp window (Dev.win_words: 8 or 16)
 constexpr int WIN_VERTS = WIN_WORDS * 32;
 
 constexpr unsigned LBL_REMOVED = 0xFFFFu;  // label of a vertex outside G': no S6 test passes
@@ -120,6 +126,7 @@ struct Dev {
   unsigned long long* sw;          // vertex state words (label | temp)
   unsigned* tbits;                 // triggered bitmap (first arrivals of the cycle)
   unsigned nwords;                 // words of the bitmap
+  unsigned win_words;              // bitmap words per warp window of the treat (8 or 16)
   unsigned* act[2];
   unsigned long long* pool[2];
   unsigned long long pool_cap;
@@ -139,6 +146,8 @@ struct Dev {
   unsigned* bnlane;                // [256] lane events per bucket
   unsigned dcap;
   int f1max;
+  unsigned long long* spill;       // [nblocks][spill_cap] events past a block's staging, per flush period
+  unsigned spill_cap;
   unsigned nblocks;                // grid size of the cycle kernels (wheel region sizing)
   // slab partition (multi-GPU / virtual slabs): local index + goff = global index
   unsigned goff;
@@ -307,8 +316,9 @@ struct Smem {
     unsigned short rank[QP_CAP];   // wheel flush: rank of an event within its delay bin
   };
   unsigned hist[WHEEL], hlane[WHEEL], rfill[WHEEL], rcap[WHEEL];
+  unsigned ofill[WHEEL];           // wheel: events appended past the staging into the open regions
   unsigned long long hbase[WHEEL], rpos[WHEEL];
-  unsigned na, np;
+  unsigned na, np, nspill;
   unsigned base_a, base_b, flag;
   View view;
   unsigned long long bhit;
@@ -592,9 +602,9 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsigned* list) {
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned wi = win * WIN_WORDS + lane;
+  const unsigned wi = win * s.win_words + lane;
   unsigned w = 0;
-  if (lane < (unsigned)WIN_WORDS && wi < s.nwords) {
+  if (lane < s.win_words && wi < s.nwords) {
     w = __ldcg(s.tbits + wi);
     if (w) s.tbits[wi] = 0u;
   }
@@ -635,8 +645,11 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #ifndef WCSP_TREAT_SCAN
 #define WCSP_TREAT_SCAN 0
 #endif
-#ifndef WCSP_FLUSH_MATCH
-#define WCSP_FLUSH_MATCH 0
+#ifndef WCSP_TREAT_PREFETCH
+#define WCSP_TREAT_PREFETCH 0
+#endif
+#ifndef WCSP_FLUSH_LAZY
+#define WCSP_FLUSH_LAZY (QP_CAP / 2)   // > 0: treat flushes its staged events only above this many
 #endif
 __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long long rec, unsigned delay, long long t);
 __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t);
@@ -755,7 +768,7 @@ template <int D, bool WHEEL_ENGINE, bool PEER = false>
 __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   Acc* acc = &s.ctl->acc[v.c % 3];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  const unsigned nwin = (s.nwords + WIN_WORDS - 1) / WIN_WORDS;
+  const unsigned nwin = (s.nwords + s.win_words - 1) / s.win_words;
   // every block owns one contiguous slab of windows: its phantoms / events come from a
   // compact region of the grid, so a run's destinations share sectors and L2 lines
   const unsigned rounds = (nwin + s.nblocks * WARPS - 1) / (s.nblocks * WARPS);
@@ -763,7 +776,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   unsigned dmin = 0xFFFFFFFFu;
   unsigned long long created = 0, relabels = 0, triggered = 0, lanes_started = 0, tested = 0;
   if constexpr (WHEEL_ENGINE) {
-    for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.rcap[d] = 0; sm.rfill[d] = 0; }
+    for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.rcap[d] = 0; sm.rfill[d] = 0; sm.ofill[d] = 0; }
     __syncthreads();
   }
   for (unsigned r = 0; r < rounds; ++r) {
@@ -771,10 +784,25 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
       const unsigned q = b + lane < total ? sm.wl[warp][b + lane] : 0xFFFFFFFFu;
+#if WCSP_TREAT_PREFETCH
+      if (b + 32 + lane < total) {   // the next batch's state word, weights and neighbours: in flight now
+        const unsigned qn = sm.wl[warp][b + 32 + lane];
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(s.sw + qn));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)s.wt + (size_t)qn * 2 * sizeof(typename Tr<D>::LW)));
+#pragma unroll
+        for (int j = 2; j < 2 * D; ++j) asm volatile("prefetch.global.L1 [%0];" ::"l"(s.sw + qn + s.off[j]));
+      }
+#endif
       treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
     }
-    if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, false);
-    else qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
+    if constexpr (WHEEL_ENGINE) {
+#if WCSP_FLUSH_LAZY
+      __syncthreads();             // flush only when the staging is half full (fewer block-wide sorts)
+      if (sm.np > (unsigned)WCSP_FLUSH_LAZY) ev_flush(s, sm, v.t, v.region, false);
+#else
+      ev_flush(s, sm, v.t, v.region, false);
+#endif
+    } else qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
   }
   if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, true);
   block_reduce_commit(sm, dmin, 0, 0, created, relabels, triggered, acc, lanes_started, tested);
@@ -912,7 +940,7 @@ __device__ __forceinline__ void load_view(const Dev& s, Smem& sm, View& v) {
 }
 
 __device__ __forceinline__ void init_smem(Smem& sm) {
-  if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; }
+  if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; sm.nspill = 0; }
   __syncthreads();
 }
 
@@ -930,7 +958,7 @@ __device__ __forceinline__ void clear_temps(const Dev& s) {
 // kernels (sweep engine)
 // ---------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) k_persistent(Dev s) {
+__global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_persistent(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
   View v;
@@ -974,7 +1002,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_persistent(Dev s) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) k_sweep(Dev s) {
+__global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_sweep(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
   View v;
@@ -988,7 +1016,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_sweep(Dev s) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) k_treat(Dev s) {
+__global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_treat(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
   View v;

@@ -29,7 +29,16 @@ namespace wcspk {
 constexpr int EV_LANE_BIT = 49;
 constexpr int EV_DELAY_SHIFT = 56;
 constexpr unsigned MAINT_PERIOD_T = 1u << 15;
-constexpr int FIRE_ITEMS = 8;             // events per lane per fire chunk (atomics in flight)
+#ifndef WCSP_FIRE_ITEMS
+#define WCSP_FIRE_ITEMS 8
+#endif
+#ifndef WCSP_FIRE_WARPS
+#define WCSP_FIRE_WARPS 8                 // warps of a block that fire events
+#endif
+#ifndef WCSP_MINB
+#define WCSP_MINB 3                       // resident blocks per SM the cycle kernels are compiled for
+#endif
+constexpr int FIRE_ITEMS = WCSP_FIRE_ITEMS;   // events per lane per fire chunk (atomics in flight)
 
 // Runs are filed per (bucket, block): the block that treats a slab of the grid
 // also fires the events its slab created, so the atomics of a fire phase
@@ -45,7 +54,22 @@ __device__ __forceinline__ void file_run(const Dev& s, unsigned b, unsigned long
 __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long long rec, unsigned delay, long long t) {
   if (idx < (unsigned)QP_CAP) {
     sm.qp[idx] = rec | ((unsigned long long)delay << EV_DELAY_SHIFT);
-  } else {                          // rare: staging full, file the event as a run of one
+    return;
+  }
+  // staging full: append to the block's open region for this delay while it has room (rfill,
+  // rcap and rpos do not change between flushes; the next flush adopts the appended events) ...
+  const unsigned k = atomicAdd(&sm.ofill[delay], 1u);
+  if (k < sm.rcap[delay] - sm.rfill[delay]) {
+    const unsigned b = (unsigned)((t + delay) & (WHEEL - 1));
+    st_hint(s.ev + ((sm.rpos[delay] + sm.rfill[delay] + k) & s.ev_mask), rec, pol_first());
+    atomicAdd(s.bnev + b, 1u);
+    if ((rec >> EV_LANE_BIT) & 1) atomicAdd(s.bnlane + b, 1u);
+    return;
+  }
+  const unsigned ks = atomicAdd(&sm.nspill, 1u);   // ... else spill it (sorted at the next flush) ...
+  if (ks < s.spill_cap) {
+    s.spill[(size_t)(blockIdx.x - s.blk0) * s.spill_cap + ks] = rec | ((unsigned long long)delay << EV_DELAY_SHIFT);
+  } else {                          // ... else file the event as a run of one (rare)
     const unsigned long long pos = atomicAdd(&s.ctl->ev_head, 1ull);
     s.ev[pos & s.ev_mask] = rec;
     const unsigned b = (unsigned)((t + delay) & (WHEEL - 1));
@@ -66,68 +90,66 @@ __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long re
   if (pred) ev_stage(s, sm, base + __popc(m & ((1u << lane) - 1u)), rec, delay, t);
 }
 
-// Counting-sort the staged events by delay and append each delay's events to
-// the block's open region for that delay (opening a new region of `region`
-// slots when it is full); final_flush files every open region.
+// Counting-sort sm.qp[0, n) by delay and append each delay's events to the
+// block's open region for that delay (opening a new region of `region` slots
+// when it is full).
+__device__ void flush_sorted(const Dev& s, Smem& sm, long long t, unsigned region, unsigned n) {
+  for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.hist[d] = 0; sm.hlane[d] = 0; }
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < n; i += THREADS) {
+    const unsigned long long e = sm.qp[i];
+    const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
+    sm.rank[i] = (unsigned short)atomicAdd(&sm.hist[d], 1u);
+    if ((e >> EV_LANE_BIT) & 1) atomicAdd(&sm.hlane[d], 1u);
+  }
+  __syncthreads();
+  for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
+    const unsigned cnt = sm.hist[d];
+    if (cnt) {
+      const unsigned b = (unsigned)((t + d) & (WHEEL - 1));
+      if (sm.rfill[d] + cnt > sm.rcap[d]) {
+        if (sm.rfill[d]) file_run(s, b, sm.rpos[d], sm.rfill[d]);
+        const unsigned size = max(region, cnt);
+        sm.rpos[d] = atomicAdd(&s.ctl->ev_head, (unsigned long long)size);
+        sm.rfill[d] = 0;
+        sm.rcap[d] = size;
+      }
+      sm.hbase[d] = sm.rpos[d] + sm.rfill[d];
+      sm.rfill[d] += cnt;
+      atomicAdd(s.bnev + b, cnt);
+      if (sm.hlane[d]) atomicAdd(s.bnlane + b, sm.hlane[d]);
+    }
+  }
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < n; i += THREADS) {
+    const unsigned long long e = sm.qp[i];
+    const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
+    st_hint(s.ev + ((sm.hbase[d] + sm.rank[i]) & s.ev_mask), e & ((1ull << EV_DELAY_SHIFT) - 1), pol_first());
+  }
+  __syncthreads();
+}
+
+// Flush the staging: events appended past it into open regions are adopted, the
+// staged events are sorted into regions, then the spilled ones (QP_CAP at a time
+// through the staging); final_flush files every open region.
 __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, bool final_flush) {
   __syncthreads();
   const unsigned n = min(sm.np, (unsigned)QP_CAP);
-  if (n > 0) {
-    for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.hist[d] = 0; sm.hlane[d] = 0; }
-    __syncthreads();
-#if !WCSP_FLUSH_MATCH
-    for (unsigned i = threadIdx.x; i < n; i += THREADS) {
-      const unsigned long long e = sm.qp[i];
-      const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
-      sm.rank[i] = (unsigned short)atomicAdd(&sm.hist[d], 1u);
-      if ((e >> EV_LANE_BIT) & 1) atomicAdd(&sm.hlane[d], 1u);
-    }
-#else
-    const unsigned lane = threadIdx.x & 31u;
-    for (unsigned i0 = threadIdx.x & ~31u; i0 < n; i0 += THREADS) {   // warp-uniform trip count
-      const unsigned i = i0 + lane;
-      const bool valid = i < n;
-      const unsigned long long e = valid ? sm.qp[i] : 0ull;
-      const unsigned d = valid ? (unsigned)(e >> EV_DELAY_SHIFT) : 0xFFFFu;
-      const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);      // lanes with the same delay
-      const int leader = __ffs(peers) - 1;
-      const unsigned lanes_in = __popc(peers & __ballot_sync(0xFFFFFFFFu, valid && ((e >> EV_LANE_BIT) & 1)));
-      unsigned base = 0;
-      if (valid && (int)lane == leader) {
-        base = atomicAdd(&sm.hist[d], (unsigned)__popc(peers));
-        if (lanes_in) atomicAdd(&sm.hlane[d], lanes_in);
-      }
-      base = __shfl_sync(0xFFFFFFFFu, base, leader);
-      if (valid) sm.rank[i] = (unsigned short)(base + __popc(peers & ((1u << lane) - 1u)));
-    }
-#endif
-    __syncthreads();
-    for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
-      const unsigned cnt = sm.hist[d];
-      if (cnt) {
-        const unsigned b = (unsigned)((t + d) & (WHEEL - 1));
-        if (sm.rfill[d] + cnt > sm.rcap[d]) {
-          if (sm.rfill[d]) file_run(s, b, sm.rpos[d], sm.rfill[d]);
-          const unsigned size = max(region, cnt);
-          sm.rpos[d] = atomicAdd(&s.ctl->ev_head, (unsigned long long)size);
-          sm.rfill[d] = 0;
-          sm.rcap[d] = size;
-        }
-        sm.hbase[d] = sm.rpos[d] + sm.rfill[d];
-        sm.rfill[d] += cnt;
-        atomicAdd(s.bnev + b, cnt);
-        if (sm.hlane[d]) atomicAdd(s.bnlane + b, sm.hlane[d]);
-      }
-    }
-    __syncthreads();
-    for (unsigned i = threadIdx.x; i < n; i += THREADS) {
-      const unsigned long long e = sm.qp[i];
-      const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
-      st_hint(s.ev + ((sm.hbase[d] + sm.rank[i]) & s.ev_mask), e & ((1ull << EV_DELAY_SHIFT) - 1), pol_first());
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) sm.np = 0;
+  const unsigned ns = min(sm.nspill, s.spill_cap);
+  for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
+    const unsigned o = sm.ofill[d];
+    if (o) { sm.rfill[d] += min(o, sm.rcap[d] - sm.rfill[d]); sm.ofill[d] = 0; }
   }
+  if (n > 0) flush_sorted(s, sm, t, region, n);
+  const unsigned long long* sp = s.spill + (size_t)(blockIdx.x - s.blk0) * s.spill_cap;
+  for (unsigned c0 = 0; c0 < ns; c0 += QP_CAP) {
+    const unsigned cn = min((unsigned)QP_CAP, ns - c0);
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < cn; i += THREADS) sm.qp[i] = __ldcg(sp + c0 + i);
+    flush_sorted(s, sm, t, region, cn);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { sm.np = 0; sm.nspill = 0; }
   if (final_flush) {
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
       if (sm.rfill[d]) file_run(s, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d]);
@@ -198,7 +220,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
     __syncthreads();
     const unsigned nchunks = dchunk[n];
     unsigned di = 0;
-    for (unsigned c = warp; c < nchunks; c += WARPS) {
+    for (unsigned c = warp; c < nchunks && warp < (unsigned)WCSP_FIRE_WARPS; c += WCSP_FIRE_WARPS) {
       while (dchunk[di + 1] <= c) ++di;          // chunks are visited in increasing order
       const unsigned long long dsc = dpos[di];
       const unsigned long long pos = dsc >> 24;
@@ -443,7 +465,7 @@ __device__ __forceinline__ bool needs_maint(const View& prev, const View& nv) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) k_wheel_persistent(Dev s) {
+__global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_persistent(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
   View v;
@@ -487,7 +509,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_wheel_persistent(Dev s) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) k_wheel_fire(Dev s) {
+__global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_fire(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
   View v;
@@ -498,7 +520,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_wheel_fire(Dev s) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) k_wheel_treat(Dev s) {
+__global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_treat(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
   View v;
@@ -605,7 +627,7 @@ __device__ __forceinline__ bool peer_sync(const Dev& s, Smem& sm, unsigned long 
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) k_wheel_peer(const __grid_constant__ DevSet set) {
+__global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_peer(const __grid_constant__ DevSet set) {
   const Dev& s = set.d[blockIdx.x / set.per];
   Smem& sm = smem();
   init_smem(sm);

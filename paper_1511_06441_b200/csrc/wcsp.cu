@@ -71,6 +71,8 @@ struct wcsp_handle {
   unsigned long long ev_cap = 0;
   unsigned long long* bdesc = nullptr;
   unsigned long long* spill = nullptr;               // [grid][spill_cap] staging overflow of the treat
+  unsigned* tlist = nullptr;                         // [grid][QA_CAP] triggered lists of the fire phase
+  unsigned* tcount = nullptr;                        // [grid]
   unsigned spill_cap = 0;
   unsigned* bcounts = nullptr;                       // bnev [256] | bnlane [256] | bndesc [256][grid]
   unsigned dcap = 0;
@@ -196,6 +198,11 @@ Dev make_dev(const wcsp_handle* h) {
   s.f1max = h->f1max;
   s.spill = h->spill;
   s.spill_cap = h->spill_cap;
+  s.tlist = h->tlist;
+  s.tcount = h->tcount;
+  // sparse cycles: about 64 triggered vertices per block (WCSP_LIST_MAX overrides, A/B runs)
+  s.list_max = getenv("WCSP_LIST_MAX") ? strtoull(getenv("WCSP_LIST_MAX"), nullptr, 10)
+                                       : (unsigned long long)h->grid * 64ull;
   s.nblocks = (unsigned)h->grid;
   s.win_words = win_words_for(s.nwords, s.nblocks);
   s.goff = h->goff;
@@ -353,7 +360,7 @@ void release(wcsp_handle* h) {
   void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->tbits, h->barr,
                   h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
                   h->d_cnt, h->d_ghost, h->g_out_lo, h->g_out_hi, h->g_in_lo, h->g_in_hi, h->l_out_lo,
-                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl, h->spill};
+                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl, h->spill, h->tlist, h->tcount};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -400,9 +407,12 @@ wcsp_status reset_ctl(wcsp_handle* h) {
   c.view.status = ST_RUNNING;
   c.view.region = 256;
   for (int i = 0; i < 3; ++i) c.acc[i].dmin = 0xFFFFFFFFu;
+  c.acc[0].tl_over = 1;            // cycle 0 treats A from the bitmap (k_init)
   CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
-  if (is_wheel(h->opt.engine))
+  if (is_wheel(h->opt.engine)) {
     CK(cudaMemsetAsync(h->bcounts, 0, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned), h->stream));
+    CK(cudaMemsetAsync(h->tcount, 0, (size_t)h->grid * sizeof(unsigned), h->stream));
+  }
   return WCSP_REACHED;
 }
 
@@ -626,6 +636,8 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
     h->spill_cap = (unsigned)std::min<unsigned long long>(16384, std::max<unsigned long long>(
                                                                      2048, pow2_at_least(8 * N / h->grid)));
     CKC(cudaMalloc(&h->spill, (size_t)h->grid * h->spill_cap * sizeof(unsigned long long)));
+    CKC(cudaMalloc(&h->tlist, (size_t)h->grid * QA_CAP * sizeof(unsigned)));
+    CKC(cudaMalloc(&h->tcount, (size_t)h->grid * sizeof(unsigned)));
   } else {
     CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
     CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));

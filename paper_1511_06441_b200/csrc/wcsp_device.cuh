@@ -67,7 +67,7 @@ struct BArr { unsigned D, cand, src, via; };   // an arrival at a target (termin
 struct Acc {                       // per-cycle accumulators, triple-buffered by cycle % 3
   unsigned n_act;                  // entries appended to the next active list
   unsigned n_pool;                 // phantoms appended to the next pool (may exceed capacity)
-  unsigned n_trig;                 // unused (kept for layout)
+  unsigned tl_over;                // wheel: first arrivals beyond some block's list went to the bitmap
   unsigned dmin;                   // min live residual after this cycle (0xFFFFFFFF = nothing live)
   unsigned long long bhit;         // max over B arrivals of (cand << 32 | ~X)
   unsigned long long live;         // sweep: live lanes at the top of the cycle (E); wheel: lanes started
@@ -85,7 +85,8 @@ struct View {                      // cycle state every block needs
   long long t;
   unsigned c, stamp, delta, n_act, n_pool;
   int cur, status;
-  unsigned region, pad_;           // timing wheel: ring region size per (block, delay)
+  unsigned region;                 // timing wheel: ring region size per (block, delay)
+  unsigned lmode;                  // timing wheel: sparse cycle, fire lists the vertices it triggers
 };
 
 struct Ctl {
@@ -147,6 +148,9 @@ struct Dev {
   unsigned dcap;
   int f1max;
   unsigned long long* spill;       // [nblocks][spill_cap] events past a block's staging, per flush period
+  unsigned* tlist;                 // [nblocks][QA_CAP] wheel: vertices a block's fire triggered (first arrivals)
+  unsigned* tcount;                // [nblocks] their number (> QA_CAP: the rest are in the bitmap)
+  unsigned long long list_max;     // a cycle is sparse (listed) if the previous one triggered at most this many
   unsigned spill_cap;
   unsigned nblocks;                // grid size of the cycle kernels (wheel region sizing)
   // slab partition (multi-GPU / virtual slabs): local index + goff = global index
@@ -463,9 +467,9 @@ __device__ __forceinline__ unsigned arrive_atomic(const Dev& s, const View& v, b
 }
 
 // src is a GLOBAL vertex index (local index + s.goff); D is local.
-template <bool PEER = false>
+template <bool PEER = false, bool LIST = false>
 __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* acc, unsigned old, unsigned D,
-                                            int cand, unsigned src, unsigned via) {
+                                            int cand, unsigned src, unsigned via, Smem* sm = nullptr) {
   const unsigned os = old >> 16;
   if (os == 0xFFFFu) {
     if (old == TMP_B) {            // termination 1°: a vertex of B is reached
@@ -480,6 +484,10 @@ __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* ac
                           ((unsigned long long)(0x7FFFFFFFu - src) << 1) | (unsigned long long)(via ? 0u : 1u));
     }
   } else if (os != v.stamp) {      // first arrival of the cycle: D is triggered (dedupe)
+    if (LIST && sm) {              // sparse cycle: the firing block lists it for its own treat while it has room
+      const unsigned k = atomicAdd(&sm->na, 1u);
+      if (k < (unsigned)QA_CAP) { sm->qa[k] = D; return; }
+    }
     if constexpr (PEER) {
       const Loc L = locate<true>(s, D);
       atom_or_sys(L.tb + (L.idx >> 5), 1u << (L.idx & 31u));
@@ -779,7 +787,24 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.rcap[d] = 0; sm.rfill[d] = 0; sm.ofill[d] = 0; }
     __syncthreads();
   }
-  for (unsigned r = 0; r < rounds; ++r) {
+  bool scan = true;
+  if constexpr (WHEEL_ENGINE) {
+    if (!s.slab && v.lmode) {      // sparse cycle: the vertices this block's fire triggered, then the bitmap if needed
+      const unsigned vb = blockIdx.x - s.blk0;
+      const unsigned cnt = min(__ldcg(s.tcount + vb), (unsigned)QA_CAP);
+      const unsigned* tl = s.tlist + (size_t)vb * QA_CAP;
+      for (unsigned b = warp * 32; b < cnt; b += WARPS * 32) {
+        const unsigned q = b + lane < cnt ? __ldcg(tl + b + lane) : 0xFFFFFFFFu;
+        treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
+      }
+      scan = __ldcg(&acc->tl_over) != 0;
+#if WCSP_FLUSH_LAZY
+      __syncthreads();
+      if (sm.np > (unsigned)WCSP_FLUSH_LAZY) ev_flush(s, sm, v.t, v.region, false);
+#endif
+    }
+  }
+  for (unsigned r = 0; scan && r < rounds; ++r) {
     const unsigned win = win0 + r * WARPS + warp;
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
@@ -812,7 +837,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
 // decide (sweep engine): Step 6 + time skipping.  One thread; writes ctl if writer.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void reset_acc(Acc* a) {
-  a->n_act = 0; a->n_pool = 0; a->n_trig = 0; a->dmin = 0xFFFFFFFFu;
+  a->n_act = 0; a->n_pool = 0; a->tl_over = 0; a->dmin = 0xFFFFFFFFu;
   a->bhit = 0; a->live = 0; a->arrivals = 0; a->created = 0; a->relabels = 0; a->triggered = 0;
   a->started = 0; a->tested = 0; a->pend_lanes = 0; a->pend_phantoms = 0;
 }
@@ -932,7 +957,7 @@ __device__ __forceinline__ void load_view(const Dev& s, Smem& sm, View& v) {
     volatile View* g = &s.ctl->view;
     View x;
     x.t = g->t; x.c = g->c; x.stamp = g->stamp; x.delta = g->delta; x.n_act = g->n_act;
-    x.n_pool = g->n_pool; x.cur = g->cur; x.status = g->status; x.region = g->region; x.pad_ = 0;
+    x.n_pool = g->n_pool; x.cur = g->cur; x.status = g->status; x.region = g->region; x.lmode = g->lmode;
     sm.view = x;
   }
   __syncthreads();

@@ -246,8 +246,20 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
         const unsigned via = ((e[it] >> EV_LANE_BIT) & 1) ? 0u : 1u;
-        arrive_post<PEER>(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu), src + s.goff,
-                          via);
+        arrive_post<PEER, !PEER>(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu),
+                                 src + s.goff, via, s.slab || !v.lmode ? nullptr : &sm);
+      }
+    }
+  }
+  if constexpr (!PEER) {            // publish the block's triggered list for its treat
+    __syncthreads();
+    if (!s.slab) {
+      const unsigned n = sm.na, m = min(n, (unsigned)QA_CAP), vb = blockIdx.x - s.blk0;
+      for (unsigned i = threadIdx.x; i < m; i += THREADS) s.tlist[(size_t)vb * QA_CAP + i] = sm.qa[i];
+      if (threadIdx.x == 0) {
+        s.tcount[vb] = m;
+        if (n > m) atomicOr(&acc->tl_over, 1u);
+        sm.na = 0;
       }
     }
   }
@@ -376,6 +388,9 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gex
     unsigned r = 128;
     while (r < per && r < 4096u) r <<= 1;
     nv.region = r;
+    // sparse cycles (thin fronts: C4, the 2-D grids) list their triggered vertices instead of
+    // having the treat scan the whole bitmap; the previous cycle's count predicts the next one's
+    nv.lmode = !s.slab && __ldcg(&a->triggered) <= s.list_max;
     if (writer) {
       if (npl + npp > C->peak_phantoms) C->peak_phantoms = npl + npp;
       C->acc[(v.c + 1) % 3].pend_lanes = npl;

@@ -1,2 +1,1 @@
-echo "== base parity"; timeout 600 python -m pytest tests -m "gpu and not slow" -x -q 2>&1 | tail -1
-for w in C3 C2 C3s P6-125 C4; do W=$w bash scripts/ab_phase.sh 2>&1 | tail -2; done
+for w in C2 C4 P6-125 C3; do W=$w ENVS="WCSP_LIST_MAX=0 WCSP_LIST_MAX=7000 WCSP_LIST_MAX=113000" bash scripts/ab_phase.sh 2>&1 | tail -8; done

@@ -609,13 +609,15 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
 // ascending vertex order (sorted processing: neighbouring Q share sectors).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsigned* list) {
+  // every lane takes 32 / lpw bits of one word (lpw lanes per word), so the serial
+  // bit extraction is short and all 32 lanes share it
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned wi = win * s.win_words + lane;
-  unsigned w = 0;
-  if (lane < s.win_words && wi < s.nwords) {
-    w = __ldcg(s.tbits + wi);
-    if (w) s.tbits[wi] = 0u;
-  }
+  const unsigned ww = s.win_words, lpw = 32u / ww, bpl = 32u / lpw;
+  const unsigned wi = win * ww + lane / lpw, sub = lane % lpw;
+  unsigned w = wi < s.nwords ? __ldcg(s.tbits + wi) : 0u;
+  __syncwarp();
+  if (sub == 0 && w) s.tbits[wi] = 0u;
+  w = (w >> (sub * bpl)) & (bpl == 32u ? 0xFFFFFFFFu : ((1u << bpl) - 1u));
   const unsigned c = __popc(w);
   unsigned x = c;
 #pragma unroll
@@ -625,8 +627,9 @@ __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsi
   }
   const unsigned total = __shfl_sync(0xFFFFFFFFu, x, 31);
   unsigned pos = x - c;
+  const unsigned vbase = wi * 32u + sub * bpl;
   while (w) {
-    list[pos++] = wi * 32u + (unsigned)(__ffs(w) - 1);
+    list[pos++] = vbase + (unsigned)(__ffs(w) - 1);
     w &= w - 1u;
   }
   __syncwarp();

@@ -32,9 +32,6 @@ constexpr unsigned MAINT_PERIOD_T = 1u << 15;
 #ifndef WCSP_FIRE_ITEMS
 #define WCSP_FIRE_ITEMS 8
 #endif
-#ifndef WCSP_FIRE_WARPS
-#define WCSP_FIRE_WARPS 8                 // warps of a block that fire events
-#endif
 #ifndef WCSP_MINB
 #define WCSP_MINB 3                       // resident blocks per SM the cycle kernels are compiled for
 #endif
@@ -219,9 +216,21 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
     }
     __syncthreads();
     const unsigned nchunks = dchunk[n];
+    // warp w fires a contiguous range of chunks (the descriptor index then advances by at most
+    // one per chunk); the first descriptor is found by binary search over the prefix sums
+    const unsigned c_lo = (unsigned)((unsigned long long)nchunks * warp / WARPS);
+    const unsigned c_hi = (unsigned)((unsigned long long)nchunks * (warp + 1) / WARPS);
     unsigned di = 0;
-    for (unsigned c = warp; c < nchunks && warp < (unsigned)WCSP_FIRE_WARPS; c += WCSP_FIRE_WARPS) {
-      while (dchunk[di + 1] <= c) ++di;          // chunks are visited in increasing order
+    {
+      unsigned lo = 0, hi = n;                   // largest di with dchunk[di] <= c_lo
+      while (hi - lo > 1) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (dchunk[mid] <= c_lo) lo = mid; else hi = mid;
+      }
+      di = lo;
+    }
+    for (unsigned c = c_lo; c < c_hi; ++c) {
+      while (dchunk[di + 1] <= c) ++di;
       const unsigned long long dsc = dpos[di];
       const unsigned long long pos = dsc >> 24;
       const unsigned cnt = (unsigned)(dsc & 0xFFFFFFu);
@@ -251,19 +260,19 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
       }
     }
   }
-  if constexpr (!PEER) {            // publish the block's triggered list for its treat
-    __syncthreads();
-    if (!s.slab) {
+  if constexpr (!PEER) {            // publish the block's triggered list for its treat (sparse cycles)
+    if (!s.slab && v.lmode) {
+      __syncthreads();
       const unsigned n = sm.na, m = min(n, (unsigned)QA_CAP), vb = blockIdx.x - s.blk0;
       for (unsigned i = threadIdx.x; i < m; i += THREADS) s.tlist[(size_t)vb * QA_CAP + i] = sm.qa[i];
       if (threadIdx.x == 0) {
         s.tcount[vb] = m;
         if (n > m) atomicOr(&acc->tl_over, 1u);
-        sm.na = 0;
       }
     }
   }
-  block_reduce_commit(sm, 0xFFFFFFFFu, 0, arr, 0, 0, 0, acc);
+  block_reduce_commit(sm, 0xFFFFFFFFu, 0, arr, 0, 0, 0, acc);   // (ends with a block barrier:
+  if (threadIdx.x == 0) sm.na = 0;                              //  every thread has read sm.na)
 }
 
 // The wheel's local proposal for the decision of cycle c (see Prop): best

@@ -1,1 +1,3 @@
-for w in C2 C4 P6-125 C3; do W=$w ENVS="WCSP_LIST_MAX=0 WCSP_LIST_MAX=7000 WCSP_LIST_MAX=113000" bash scripts/ab_phase.sh 2>&1 | tail -8; done
+echo "== base parity"; timeout 900 python -m pytest tests -m "gpu" -x -q 2>&1 | tail -1
+echo "== QP_CAP256 parity"; WCSP_LIB=paper_1511_06441_b200/libwcsp_QP_CAP256.so timeout 600 python -m pytest tests -m "gpu and not slow" -x -q 2>&1 | tail -1
+timeout 250 python scripts/peer_det.py

@@ -445,3 +445,17 @@ def test_slab_handle_reuse_across_budgets(halo):
                 fresh = wcsp.solve(inst.with_M(M), engine="wheel", slabs=3, halo=halo)
                 assert r.key() == fresh.key() == oracle.solve_pruned(inst.with_M(M)).key()
                 assert model_counters(r) == model_counters(fresh)
+
+
+def test_counters_stable_over_repeats():
+    """Repeated solves (sparse cycles with per-block triggered lists, dense
+    cycles with the bitmap, both engines) give tier 5's counters every time —
+    a race between blocks would show up as a run-to-run difference."""
+    for inst in (I.config_face((48, 48, 48), 0, 260), I.fractal_instance(7), I.config_face((200, 200), 6, 700)):
+        m, mc = oracle.solve_model(inst)
+        want = (mc.cycles, mc.work, mc.arrivals, mc.triggered, mc.created, mc.started, mc.relabels)
+        for engine in ("wheel", "wheel_stepped", "persistent"):
+            with wcsp.Solver(inst, engine=engine) as s:
+                for _ in range(6):
+                    r = s.solve()
+                    assert r.key() == m.key() and model_counters(r) == want, (inst.name, engine, r)

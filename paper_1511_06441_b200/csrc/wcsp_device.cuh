@@ -323,6 +323,8 @@ struct Smem {
   unsigned ofill[WHEEL];           // wheel: events appended past the staging into the open regions
   unsigned long long hbase[WHEEL], rpos[WHEEL];
   unsigned na, np, nspill;
+  unsigned bm_lo, bm_words;        // wheel fire, dense cycles: the block's triggered bitmap in qp covers
+                                   // vertices [bm_lo, bm_lo + 32 * bm_words)
   unsigned base_a, base_b, flag;
   View view;
   unsigned long long bhit;
@@ -484,9 +486,17 @@ __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* ac
                           ((unsigned long long)(0x7FFFFFFFu - src) << 1) | (unsigned long long)(via ? 0u : 1u));
     }
   } else if (os != v.stamp) {      // first arrival of the cycle: D is triggered (dedupe)
-    if (LIST && sm) {              // sparse cycle: the firing block lists it for its own treat while it has room
-      const unsigned k = atomicAdd(&sm->na, 1u);
-      if (k < (unsigned)QA_CAP) { sm->qa[k] = D; return; }
+    if (LIST && sm) {
+      if (v.lmode) {               // sparse cycle: the firing block lists it for its own treat while it has room
+        const unsigned k = atomicAdd(&sm->na, 1u);
+        if (k < (unsigned)QA_CAP) { sm->qa[k] = D; return; }
+      } else {                     // dense cycle: near the block's own slab, a shared-memory bit first
+        const unsigned r = D - sm->bm_lo;
+        if (r < sm->bm_words * 32u) {
+          atomicOr(reinterpret_cast<unsigned*>(sm->qp) + (r >> 5), 1u << (r & 31u));
+          return;
+        }
+      }
     }
     if constexpr (PEER) {
       const Loc L = locate<true>(s, D);

@@ -189,6 +189,30 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   unsigned* dchunk = &sm.wl[0][0] + 2 * MAXD;                                         // [MAXD + 1] prefix
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   unsigned long long arr = 0;
+  // Dense cycles: first arrivals near the block's own slab of the grid (its treat windows and one
+  // plane of the last axis on either side: where the events it fires lead) set bits of a
+  // shared-memory bitmap (the treat staging is free during the fire), merged into the global
+  // bitmap with one atomicOr per word at the end; sparse cycles list them (see arrive_post).
+  const bool local_bits = !PEER && !s.slab && !v.lmode;
+  if (local_bits) {
+    if (threadIdx.x == 0) {
+      const unsigned long long ww = s.win_words, nwin = (s.nwords + ww - 1) / ww;
+      const unsigned long long rounds = (nwin + (unsigned long long)s.nblocks * WARPS - 1) / ((unsigned long long)s.nblocks * WARPS);
+      const unsigned long long span = rounds * WARPS * ww * 32ull;
+      const unsigned long long vlo = (unsigned long long)(blockIdx.x - s.blk0) * span;
+      const unsigned long long vhi = min((unsigned long long)s.N, vlo + span);
+      const unsigned long long S = s.off[s.NL - 2], cap = (unsigned long long)QP_CAP * 64ull;
+      unsigned long long lo = vlo >= S ? vlo - S : 0ull, hi = min((unsigned long long)s.N, vhi + S);
+      if (hi - lo + 32 > cap) { lo = vlo; hi = vhi; }
+      if (vlo >= vhi || hi - lo + 32 > cap) { lo = 0; hi = 0; }
+      lo &= ~31ull;
+      sm.bm_lo = (unsigned)lo;
+      sm.bm_words = (unsigned)((hi - lo + 31) / 32);
+    }
+    __syncthreads();
+    unsigned* bm = reinterpret_cast<unsigned*>(sm.qp);
+    for (unsigned i = threadIdx.x; i < sm.bm_words; i += THREADS) bm[i] = 0u;
+  }
   for (unsigned d0 = 0; d0 < nd; d0 += MAXD) {
     const unsigned n = min(MAXD, nd - d0);
     __syncthreads();
@@ -256,8 +280,17 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
         const unsigned via = ((e[it] >> EV_LANE_BIT) & 1) ? 0u : 1u;
         arrive_post<PEER, !PEER>(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu),
-                                 src + s.goff, via, s.slab || !v.lmode ? nullptr : &sm);
+                                 src + s.goff, via, s.slab ? nullptr : &sm);
       }
+    }
+  }
+  if (local_bits) {                 // merge the shared-memory bitmap
+    __syncthreads();
+    const unsigned* bm = reinterpret_cast<const unsigned*>(sm.qp);
+    const unsigned w0 = sm.bm_lo >> 5;
+    for (unsigned i = threadIdx.x; i < sm.bm_words; i += THREADS) {
+      const unsigned w = bm[i];
+      if (w) atomicOr(s.tbits + w0 + i, w);
     }
   }
   if constexpr (!PEER) {            // publish the block's triggered list for its treat (sparse cycles)

@@ -633,8 +633,8 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
     CKC(cudaMalloc(&h->bcounts, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned)));
     // spill room per block and flush period: a dense window round (e.g. the initial treatment
     // of a whole boundary) can stage several times the shared-memory staging
-    h->spill_cap = (unsigned)std::min<unsigned long long>(16384, std::max<unsigned long long>(
-                                                                     2048, pow2_at_least(8 * N / h->grid)));
+    h->spill_cap = (unsigned)std::min<unsigned long long>(WCSP_FLUSH_LAZY < 0 ? 65536 : 16384,
+                                                          std::max<unsigned long long>(2048, pow2_at_least(8 * N / h->grid)));
     CKC(cudaMalloc(&h->spill, (size_t)h->grid * h->spill_cap * sizeof(unsigned long long)));
     CKC(cudaMalloc(&h->tlist, (size_t)h->grid * QA_CAP * sizeof(unsigned)));
     CKC(cudaMalloc(&h->tcount, (size_t)h->grid * sizeof(unsigned)));

@@ -666,8 +666,8 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #ifndef WCSP_TREAT_SCAN
 #define WCSP_TREAT_SCAN 0
 #endif
-#ifndef WCSP_TREAT_PREFETCH
-#define WCSP_TREAT_PREFETCH 0
+#ifndef WCSP_TREAT_EAGER
+#define WCSP_TREAT_EAGER 0         // 1: issue the neighbour loads together with Q's own (measured: no gain on C3)
 #endif
 #ifndef WCSP_FLUSH_LAZY
 #define WCSP_FLUSH_LAZY (QP_CAP / 2)   // > 0: treat flushes its staged events only above this many
@@ -685,6 +685,16 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
   tested += valid;
   const unsigned long long swq = valid ? ld_hint(s.sw + q, pol_last()) : 0ull;
   const WRec<LW> wr = valid ? load_wt_cs<D>(s, q) : WRec<LW>{0, 0};
+  unsigned long long swr[2 * D];
+#if WCSP_TREAT_EAGER
+  if constexpr (!PEER) {             // neighbours loaded with Q's own words: one memory round trip
+#pragma unroll
+    for (int j = 0; j < 2 * D; ++j) {
+      const unsigned u = q + s.off[j];
+      swr[j] = valid && u < s.N ? s.sw[u] : 0xFFFFull;
+    }
+  }
+#endif
   LW w = 0;
   if constexpr (!WHEEL_ENGINE) w = valid ? __ldcg(reinterpret_cast<LW*>(s.res) + q) : (LW)0;
   const int lq = (int)(swq & 0xFFFFu);
@@ -694,12 +704,17 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
   if constexpr (WHEEL_ENGINE) inactive = trig && !lane_live((unsigned)(swq >> 16) & 0xFFFFu, v.t);
   else inactive = trig && w == 0;                                 // no live lane after the decrement (R6)
   triggered += trig;
-  unsigned long long swr[2 * D];
 #pragma unroll
   for (int j = 0; j < 2 * D; ++j) {
     const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
     const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
     const bool test = trig && f1j != 0 && lstar - (int)f2j > 0;
+#if WCSP_TREAT_EAGER
+    if constexpr (!PEER) {
+      if (!test) swr[j] = 0xFFFFull;   // untested lanes read as "removed"
+      continue;
+    }
+#endif
     // L1-cached read: this phase never writes the temp half, the label half only moves to
     // max(L, temp) (benign), and the grid barrier before the phase invalidated L1
     if constexpr (PEER) {            // a neighbour in the next slab is read in its owner's memory
@@ -811,7 +826,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
         treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
       }
       scan = __ldcg(&acc->tl_over) != 0;
-#if WCSP_FLUSH_LAZY
+#if WCSP_FLUSH_LAZY > 0
       __syncthreads();
       if (sm.np > (unsigned)WCSP_FLUSH_LAZY) ev_flush(s, sm, v.t, v.region, false);
 #endif
@@ -822,24 +837,15 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
       const unsigned q = b + lane < total ? sm.wl[warp][b + lane] : 0xFFFFFFFFu;
-#if WCSP_TREAT_PREFETCH
-      if (b + 32 + lane < total) {   // the next batch's state word, weights and neighbours: in flight now
-        const unsigned qn = sm.wl[warp][b + 32 + lane];
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(s.sw + qn));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)s.wt + (size_t)qn * 2 * sizeof(typename Tr<D>::LW)));
-#pragma unroll
-        for (int j = 2; j < 2 * D; ++j) asm volatile("prefetch.global.L1 [%0];" ::"l"(s.sw + qn + s.off[j]));
-      }
-#endif
       treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
     }
     if constexpr (WHEEL_ENGINE) {
-#if WCSP_FLUSH_LAZY
+#if WCSP_FLUSH_LAZY > 0
       __syncthreads();             // flush only when the staging is half full (fewer block-wide sorts)
       if (sm.np > (unsigned)WCSP_FLUSH_LAZY) ev_flush(s, sm, v.t, v.region, false);
-#else
+#elif WCSP_FLUSH_LAZY == 0
       ev_flush(s, sm, v.t, v.region, false);
-#endif
+#endif                             // < 0: no block barrier between rounds; overflow spills, one flush at the end
     } else qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
   }
   if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, true);

@@ -16,7 +16,7 @@ import oracle  # noqa: E402
 from paper_1511_06441_b200 import instances as I  # noqa: E402
 
 OUT = os.path.join(ROOT, "paper_1511_06441_b200", "data", "mbind.json")
-SHAPES = {"C2": (1024, 1024), "C3": (256, 256, 256), "C3s": (128, 128, 128),
+SHAPES = {"C2": (1024, 1024), "C3": (256, 256, 256), "C3s": (128, 128, 128), "C5": (1024, 1024, 1024),
           # §6 protocol: water on the cube's boundary, B = the centre vertex
           "P6-50": (50, 50, 50), "P6-75": (75, 75, 75), "P6-100": (100, 100, 100), "P6-125": (125, 125, 125)}
 

@@ -151,7 +151,7 @@ cudaError_t set_smem_attrs() {
 // words when that gives at most one round or at least four (C2, C3), else 8 (C3s, P6 cubes).
 // WCSP_WIN_WORDS overrides (A/B runs).
 unsigned win_words_for(unsigned nwords, unsigned nblocks) {
-  if (const char* e = getenv("WCSP_WIN_WORDS")) return atoi(e) >= 16 ? 16u : 8u;
+  if (const char* e = getenv("WCSP_WIN_WORDS")) return atoi(e) >= WIN_WORDS ? (unsigned)WIN_WORDS : atoi(e) >= 16 ? 16u : 8u;
   if (nblocks == 0) return 8u;
   const double rounds16 = (double)nwords / (16.0 * nblocks * WARPS);
   return rounds16 <= 1.0 || rounds16 >= 4.0 ? 16u : 8u;
@@ -1057,9 +1057,7 @@ wcsp_status dist_cycle(wcsp_handle* g, const Dev& dv) {
 
 wcsp_status dist_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
   wcsp_status st;
-  NcclApi& nc = nccl_api();
   wcsp_handle* c = g->children[0];
-  ncclComm_t comm = (ncclComm_t)g->comm;
   g->launches = 0;
   CK(cudaEventRecord(g->e0, g->stream));
   c->M = g->M;

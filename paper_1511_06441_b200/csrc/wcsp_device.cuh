@@ -46,7 +46,10 @@ constexpr int CHUNK_MAX = THREADS * SWEEP_ITEMS;
 #endif
 constexpr int QP_CAP = WCSP_QP_CAP;             // shared staging of phantoms / events (overflow -> direct append)
 constexpr int QA_CAP = 2048;             // shared staging of active-list appends (never overflows)
-constexpr int WIN_WORDS = 16;            // max triggered-bitmap words per warp window (Dev.win_words: 8 or 16)
+#ifndef WCSP_WIN_MAX
+#define WCSP_WIN_MAX 16
+#endif
+constexpr int WIN_WORDS = WCSP_WIN_MAX;  // max triggered-bitmap words per warp window (Dev.win_words: 8 or 16)
 constexpr int WIN_VERTS = WIN_WORDS * 32;
 
 constexpr unsigned LBL_REMOVED = 0xFFFFu;  // label of a vertex outside G': no S6 test passes
@@ -663,9 +666,6 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 
 // Stage events for the wheel (defined in wcsp_wheel.cuh): at a reserved staging slot, or
 // one per predicated lane (warp-aggregated).
-#ifndef WCSP_TREAT_SCAN
-#define WCSP_TREAT_SCAN 0
-#endif
 #ifndef WCSP_TREAT_EAGER
 #define WCSP_TREAT_EAGER 0         // 1: issue the neighbour loads together with Q's own (measured: no gain on C3)
 #endif
@@ -725,7 +725,7 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     }
   }
   LW neww = 0;
-  unsigned fmax = 0, pm = 0;
+  unsigned fmax = 0;
 #pragma unroll
   for (int j = 0; j < 2 * D; ++j) {
     const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
@@ -740,14 +740,10 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     lanes_started += pass && inactive;                            // activate, time restored to f1 (:192)
     if constexpr (WHEEL_ENGINE) {
       if (pass && inactive) fmax = max(fmax, f1j);
-#if WCSP_TREAT_SCAN
-      if (pass) pm |= 1u << j;
-#else
       const unsigned long long rec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
                                      ((unsigned long long)(unsigned)c << PH_CAND) |
                                      ((unsigned long long)(inactive ? 1u : 0u) << 49);
       ev_push(s, sm, pass, rec, f1j, v.t);
-#endif
     } else {
       if (pass) dmin = min(dmin, f1j);
       if (pass && inactive) neww |= (LW)f1j << (8 * j);
@@ -757,32 +753,6 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       qpush<unsigned long long>(sm.qp, QP_CAP, &sm.np, ph, prec, &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
     }
   }
-#if WCSP_TREAT_SCAN
-  if constexpr (WHEEL_ENGINE) {     // one warp-level reservation for all of this Q's new edges
-    const unsigned lane = threadIdx.x & 31u, cnt = __popc(pm);
-    unsigned x = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-      if ((int)lane >= o) x += y;
-    }
-    const unsigned total = __shfl_sync(0xFFFFFFFFu, x, 31);
-    unsigned base = 0;
-    if (lane == 31 && total) base = atomicAdd(&sm.np, total);
-    base = __shfl_sync(0xFFFFFFFFu, base, 31);
-    unsigned pos = base + x - cnt;
-    while (pm) {
-      const int j = __ffs(pm) - 1;
-      pm &= pm - 1u;
-      const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
-      const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
-      const unsigned long long rec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
-                                     ((unsigned long long)(unsigned)(lstar - (int)f2j) << PH_CAND) |
-                                     ((unsigned long long)(inactive ? 1u : 0u) << 49);
-      ev_stage(s, sm, pos++, rec, f1j, v.t);
-    }
-  }
-#endif
   if (inactive) {                                                 // Step 8.1
     relabels += 1;
     if constexpr (WHEEL_ENGINE) {

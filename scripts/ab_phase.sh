@@ -7,5 +7,5 @@ for v in base ${VARIANTS}; do
   echo "== $v"; WCSP_L2_PERSIST=0 WCSP_LIB=$lib python scripts/phase_breakdown.py $W wheel 2>&1 | grep '"cycle_ms"'
 done
 for e in ${ENVS}; do
-  echo "== env $e"; env WCSP_L2_PERSIST=0 $e python scripts/phase_breakdown.py $W wheel 2>&1 | grep '"cycle_ms"'
+  echo "== env $e"; env WCSP_L2_PERSIST=0 ${e//:/ } python scripts/phase_breakdown.py $W wheel 2>&1 | grep '"cycle_ms"'
 done

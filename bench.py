@@ -37,6 +37,9 @@ WORKLOADS = {
     "C2": {"shape": (1024, 1024), "desc": "configs[1]: 2D 1024^2, f1,f2 ~ U{1..10}, A = left face, B = right face, "
                                           "M = M_bind"},
     "C3s": {"shape": (128, 128, 128), "desc": "128^3 cube (reduced C3 for quick runs), M = M_bind"},
+    "C5": {"shape": (1024, 1024, 1024), "desc": "configs[4]: 3D 1024^3 cube, f1,f2 ~ U{1..10}, face x=0 -> face "
+                                                "x=1023, M = M_bind; unsliced on one B200 (about 105 GB of HBM) or "
+                                                "z-slabs over N GPUs with --partition slabs"},
     "C4": {"shape": None, "desc": "configs[3]: Theorem-2 fractal omega_k, k = 10 (t = 1024), V = [-t,t]x[0,t+1], "
                                   "A = x-axis, B = (0,t), f1 in {1,2}, f2 = 1, M = infinity"},
 }

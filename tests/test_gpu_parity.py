@@ -459,3 +459,46 @@ def test_counters_stable_over_repeats():
                 for _ in range(6):
                     r = s.solve()
                     assert r.key() == m.key() and model_counters(r) == want, (inst.name, engine, r)
+
+
+# --- extremes: full u8 weights, the largest budget, long times (texp refresh, stamp wrap), thin grids ---
+
+def test_extreme_weights_and_budgets():
+    """f1, f2 over the whole u8 range (1..255: the wheel's 256 buckets, times
+    past 2^16 so the lane-expiry refresh runs), M from 1 to WCSP_M_MAX, and
+    degenerate shapes (axes of length 1, one-row grids): outputs vs the oracle,
+    counters vs tier 5."""
+    rng = np.random.default_rng(1717)
+    shapes = [(40, 40), (1, 60), (60, 1), (9, 1, 9), (400,), (7, 7, 7), (2, 2, 2, 30), (1, 1, 1, 50)]
+    cases = 0
+    for i in range(40):
+        shape = shapes[i % len(shapes)]
+        lo, hi = [(200, 255), (1, 255), (128, 255)][i % 3]
+        inst = I.random_small(rng, shapes=[shape], lo_hi=(lo, hi), M_range=(1, wcsp.M_MAX),
+                              max_sources=3, max_targets=3)
+        if i % 4 == 0:
+            inst = inst.with_M(wcsp.M_MAX)
+        if i % 4 == 1:
+            inst = inst.with_M(I.M_INF)
+        if i % 8 == 2:
+            inst = inst.with_M(1)
+        for engine in ("wheel", "persistent"):
+            check(inst, engine)
+        cases += 1
+    # one long line: F1 > 2^16 time units with f1 = 255 everywhere
+    s = I.grid_instance((300,), 3, 255, 255, "corner0", "corner1", I.M_INF, "line255")
+    r, _ = check(s, "wheel")
+    assert r.F1 == 255 * 299 and r.F1 > (1 << 16)
+    assert cases == 40
+
+
+@pytest.mark.parametrize("engine", ["wheel", "persistent"])
+def test_stamp_wrap_long_run(engine):
+    """More than 65534 cycles (the 16-bit cycle stamps wrap, PAPER.md:133's
+    'temporary label' is reset by the maintenance pass): a 1-D line of
+    70000 unit edges in unit time."""
+    n = 70000
+    s = I.grid_instance((n,), 5, 1, 1, "corner0", "corner1", I.M_INF, "line1")
+    r = wcsp.solve(s, engine=engine, time_mode="unit")
+    assert r.key() == oracle.solve_lex(s, 2).key()
+    assert r.F1 == n - 1 and r.cycles == n - 1

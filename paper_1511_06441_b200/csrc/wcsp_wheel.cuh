@@ -32,6 +32,10 @@ constexpr unsigned MAINT_PERIOD_T = 1u << 15;
 #ifndef WCSP_FIRE_ITEMS
 #define WCSP_FIRE_ITEMS 8
 #endif
+#ifndef WCSP_FIRE_PRECHECK
+#define WCSP_FIRE_PRECHECK 0              // 1: skip atomics an L1 copy of the state word shows to be no-ops
+                                          //    (measured: treat -6 %, fire +35 % on C3 -- off)
+#endif
 #ifndef WCSP_MINB
 #define WCSP_MINB 3                       // resident blocks per SM the cycle kernels are compiled for
 #endif
@@ -266,12 +270,43 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         e[it] = i < cnt ? ld_hint(s.ev + ((pos + i) & s.ev_mask), pol_first()) : ~0ull;
       }
       unsigned old[FIRE_ITEMS];
+#if WCSP_FIRE_PRECHECK
+      // An arrival that cannot change temp(D) needs no atomic: labels only grow and temps only
+      // grow within a cycle, so if an L1 copy of D's state word (possibly stale, never too
+      // high) already holds L(D) >= cand, or a temp of this cycle >= cand, the atomic would
+      // be a no-op (and D's first arrival has happened or cannot trigger it).  Sentinel temps
+      // (targets, removed, ghosts) are never skipped on the temp rule; removed labels skip.
+      bool skip[FIRE_ITEMS];
+      if constexpr (!PEER) {
+        unsigned long long w[FIRE_ITEMS];
+#pragma unroll
+        for (int it = 0; it < FIRE_ITEMS; ++it) {
+          const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
+          const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
+          w[it] = e[it] != ~0ull ? s.sw[src + s.off[ln]] : 0ull;
+        }
+#pragma unroll
+        for (int it = 0; it < FIRE_ITEMS; ++it) {
+          const unsigned cand = (unsigned)(e[it] >> PH_CAND) & 0xFFFFu;
+          const unsigned tw = (unsigned)(w[it] >> 32);
+          skip[it] = e[it] != ~0ull && (((unsigned)w[it] & 0xFFFFu) >= cand ||
+                                        ((tw >> 16) == v.stamp && (tw & 0xFFFFu) >= cand));
+        }
+      }
+#endif
 #pragma unroll
       for (int it = 0; it < FIRE_ITEMS; ++it) {   // put every atomic in flight before using a result
         const bool valid = e[it] != ~0ull;
         arr += valid;
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
+#if WCSP_FIRE_PRECHECK
+        if constexpr (!PEER) {
+          old[it] = arrive_atomic<PEER>(s, v, valid && !skip[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));
+          if (skip[it]) old[it] = v.stamp << 16;   // as if a later arrival of this cycle: nothing to do
+          continue;
+        }
+#endif
         old[it] = arrive_atomic<PEER>(s, v, valid, src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));
       }
 #pragma unroll

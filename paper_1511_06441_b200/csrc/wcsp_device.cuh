@@ -495,7 +495,7 @@ __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* ac
         if (k < (unsigned)QA_CAP) { sm->qa[k] = D; return; }
       } else {                     // dense cycle: near the block's own slab, a shared-memory bit first
         const unsigned r = D - sm->bm_lo;
-        if (r < sm->bm_words * 32u) {
+        if (r < sm->bm_words * 32u && (!PEER || (D >= s.plo_end && D < s.ghost_hi_start))) {
           atomicOr(reinterpret_cast<unsigned*>(sm->qp) + (r >> 5), 1u << (r & 31u));
           return;
         }

@@ -197,7 +197,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   // plane of the last axis on either side: where the events it fires lead) set bits of a
   // shared-memory bitmap (the treat staging is free during the fire), merged into the global
   // bitmap with one atomicOr per word at the end; sparse cycles list them (see arrive_post).
-  const bool local_bits = !PEER && !s.slab && !v.lmode;
+  const bool local_bits = (PEER || !s.slab) && !v.lmode;
   if (local_bits) {
     if (threadIdx.x == 0) {
       const unsigned long long ww = s.win_words, nwin = (s.nwords + ww - 1) / ww;
@@ -207,8 +207,12 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
       const unsigned long long vhi = min((unsigned long long)s.N, vlo + span);
       const unsigned long long S = s.off[s.NL - 2], cap = (unsigned long long)QP_CAP * 64ull;
       unsigned long long lo = vlo >= S ? vlo - S : 0ull, hi = min((unsigned long long)s.N, vhi + S);
+      if (PEER) {                  // never a ghost plane: those are the neighbours' vertices
+        lo = max(lo, (unsigned long long)s.plo_end);
+        hi = min(hi, (unsigned long long)s.ghost_hi_start);
+      }
       if (hi - lo + 32 > cap) { lo = vlo; hi = vhi; }
-      if (vlo >= vhi || hi - lo + 32 > cap) { lo = 0; hi = 0; }
+      if (vlo >= vhi || hi <= lo || hi - lo + 32 > cap) { lo = 0; hi = 0; }
       lo &= ~31ull;
       sm.bm_lo = (unsigned)lo;
       sm.bm_words = (unsigned)((hi - lo + 31) / 32);
@@ -314,8 +318,8 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
         const unsigned via = ((e[it] >> EV_LANE_BIT) & 1) ? 0u : 1u;
-        arrive_post<PEER, !PEER>(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu),
-                                 src + s.goff, via, s.slab ? nullptr : &sm);
+        arrive_post<PEER, true>(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu),
+                                src + s.goff, via, local_bits || (!s.slab && v.lmode) ? &sm : nullptr);
       }
     }
   }
@@ -325,7 +329,10 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
     const unsigned w0 = sm.bm_lo >> 5;
     for (unsigned i = threadIdx.x; i < sm.bm_words; i += THREADS) {
       const unsigned w = bm[i];
-      if (w) atomicOr(s.tbits + w0 + i, w);
+      if (w) {
+        if constexpr (PEER) atom_or_sys(s.tbits + w0 + i, w);   // the neighbours OR into it too
+        else atomicOr(s.tbits + w0 + i, w);
+      }
     }
   }
   if constexpr (!PEER) {            // publish the block's triggered list for its treat (sparse cycles)
@@ -667,8 +674,11 @@ __device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
 }
 
+// propose: the leader, once every block of its slab has arrived (the slab's treat is
+// complete), writes the slab's proposal for the cycle decision before joining the other
+// slabs, so one barrier both ends the treat and publishes the proposals.
 __device__ __forceinline__ bool peer_sync(const Dev& s, Smem& sm, unsigned long long epoch,
-                                          unsigned long long* fin = nullptr) {
+                                          unsigned long long* fin = nullptr, const View* propose = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     if (fin) {
@@ -695,6 +705,10 @@ __device__ __forceinline__ bool peer_sync(const Dev& s, Smem& sm, unsigned long 
         if (timed_out()) { ok = 0; break; }
       }
       if (ok) {
+        if (propose) {
+          long long need = 0;
+          s.ctl->prop = wheel_propose(s, *propose, &need);
+        }
         __threadfence_system();
         red_add_release_sys(s.xbar, 1ull);
         while (ld_acquire_sys(s.xbar) < epoch * (unsigned long long)s.nslab) {
@@ -746,13 +760,9 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_peer(const __grid_
     if (!bhit) {
       if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
       phase_treat<D, true, true>(s, v, sm);
-      if (!peer_sync(s, sm, ++epoch, &s.ctl->fin[v.c & 1][1][0])) return;
     }
-    if (leader && threadIdx.x == 0) {   // this slab's proposal for the decision
-      long long need = 0;
-      s.ctl->prop = wheel_propose(s, v, &need);
-    }
-    if (!peer_sync(s, sm, ++epoch)) return;
+    // end of the treat + every slab's proposal for the decision, in one barrier
+    if (!peer_sync(s, sm, ++epoch, bhit ? nullptr : &s.ctl->fin[v.c & 1][1][0], &v)) return;
     const View prev = v;
     if (threadIdx.x == 0) {          // every slab takes the same decision from the combined proposal
       Prop G{0, -(long long)WHEEL, 0, 0};

@@ -325,6 +325,14 @@ struct Smem {
   unsigned hist[WHEEL], hlane[WHEEL], rfill[WHEEL], rcap[WHEEL];
   unsigned ofill[WHEEL];           // wheel: events appended past the staging into the open regions
   unsigned long long hbase[WHEEL], rpos[WHEEL];
+#if WCSP_WARP_FLUSH
+  // warp-level event filing: warp w stages in qp[w * WQ, (w + 1) * WQ) and files its own
+  // events into the block's open regions (per-delay locks) without block barriers
+  unsigned wnp[WARPS];
+  unsigned whist[WARPS][WHEEL];    // (count | lane events << 16), then the ring index of the delay's slot
+  unsigned short wrank[QP_CAP];
+  int rlock[WHEEL];
+#endif
   unsigned na, np, nspill;
   unsigned bm_lo, bm_words;        // wheel fire, dense cycles: the block's triggered bitmap in qp covers
                                    // vertices [bm_lo, bm_lo + 32 * bm_words)
@@ -669,11 +677,19 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #ifndef WCSP_TREAT_EAGER
 #define WCSP_TREAT_EAGER 0         // 1: issue the neighbour loads together with Q's own (measured: no gain on C3)
 #endif
+#ifndef WCSP_WARP_FLUSH
+#define WCSP_WARP_FLUSH 0          // 1: every warp files its own events (no block barriers in the treat);
+                                   //    measured on C3: treat +9 %, fire +64 % (interleaved runs) -- off
+#endif
 #ifndef WCSP_FLUSH_LAZY
 #define WCSP_FLUSH_LAZY (QP_CAP / 2)   // > 0: treat flushes its staged events only above this many
 #endif
 __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long long rec, unsigned delay, long long t);
 __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t);
+__device__ void ev_push_warp(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t,
+                             unsigned region);
+__device__ void warp_flush(const Dev& s, Smem& sm, long long t, unsigned region);
+__device__ void regions_close(const Dev& s, Smem& sm, long long t);
 
 template <int D, bool WHEEL_ENGINE, bool PEER>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
@@ -743,7 +759,11 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       const unsigned long long rec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
                                      ((unsigned long long)(unsigned)c << PH_CAND) |
                                      ((unsigned long long)(inactive ? 1u : 0u) << 49);
+#if WCSP_WARP_FLUSH
+      ev_push_warp(s, sm, pass, rec, f1j, v.t, v.region);
+#else
       ev_push(s, sm, pass, rec, f1j, v.t);
+#endif
     } else {
       if (pass) dmin = min(dmin, f1j);
       if (pass && inactive) neww |= (LW)f1j << (8 * j);
@@ -782,7 +802,15 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   unsigned dmin = 0xFFFFFFFFu;
   unsigned long long created = 0, relabels = 0, triggered = 0, lanes_started = 0, tested = 0;
   if constexpr (WHEEL_ENGINE) {
-    for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) { sm.rcap[d] = 0; sm.rfill[d] = 0; sm.ofill[d] = 0; }
+    for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
+      sm.rcap[d] = 0; sm.rfill[d] = 0; sm.ofill[d] = 0;
+#if WCSP_WARP_FLUSH
+      sm.rlock[d] = 0;
+#endif
+    }
+#if WCSP_WARP_FLUSH
+    if (threadIdx.x < WARPS) sm.wnp[threadIdx.x] = 0;
+#endif
     __syncthreads();
   }
   bool scan = true;
@@ -796,7 +824,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
         treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
       }
       scan = __ldcg(&acc->tl_over) != 0;
-#if WCSP_FLUSH_LAZY > 0
+#if WCSP_FLUSH_LAZY > 0 && !WCSP_WARP_FLUSH
       __syncthreads();
       if (sm.np > (unsigned)WCSP_FLUSH_LAZY) ev_flush(s, sm, v.t, v.region, false);
 #endif
@@ -810,7 +838,9 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
       treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
     }
     if constexpr (WHEEL_ENGINE) {
-#if WCSP_FLUSH_LAZY > 0
+#if WCSP_WARP_FLUSH
+      // nothing: every warp files its own events as its staging fills
+#elif WCSP_FLUSH_LAZY > 0
       __syncthreads();             // flush only when the staging is half full (fewer block-wide sorts)
       if (sm.np > (unsigned)WCSP_FLUSH_LAZY) ev_flush(s, sm, v.t, v.region, false);
 #elif WCSP_FLUSH_LAZY == 0
@@ -818,7 +848,14 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
 #endif                             // < 0: no block barrier between rounds; overflow spills, one flush at the end
     } else qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
   }
-  if constexpr (WHEEL_ENGINE) ev_flush(s, sm, v.t, v.region, true);
+  if constexpr (WHEEL_ENGINE) {
+#if WCSP_WARP_FLUSH
+    warp_flush(s, sm, v.t, v.region);
+    regions_close(s, sm, v.t);
+#else
+    ev_flush(s, sm, v.t, v.region, true);
+#endif
+  }
   block_reduce_commit(sm, dmin, 0, 0, created, relabels, triggered, acc, lanes_started, tested);
 }
 

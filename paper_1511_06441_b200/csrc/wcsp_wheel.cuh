@@ -91,6 +91,91 @@ __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long re
   if (pred) ev_stage(s, sm, base + __popc(m & ((1u << lane) - 1u)), rec, delay, t);
 }
 
+#if WCSP_WARP_FLUSH
+constexpr unsigned WQ = QP_CAP / WARPS;   // staging slots per warp
+
+// Warp-level filing: the calling warp sorts its staged events by delay (warp-private
+// histogram and ranks), reserves each delay's slots in the block's open region for that
+// delay under a per-delay lock (opening a new region — and filing the full one as a run —
+// when it has no room), and writes its events.  Only __syncwarp; other warps go on.
+__device__ void warp_flush(const Dev& s, Smem& sm, long long t, unsigned region) {
+  const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const unsigned n = sm.wnp[w];
+  if (n == 0) return;
+  unsigned* hist = sm.whist[w];
+  const unsigned long long* q = sm.qp + (size_t)w * WQ;
+  unsigned short* rk = sm.wrank + (size_t)w * WQ;
+  for (unsigned d = lane; d < WHEEL; d += 32) hist[d] = 0;
+  __syncwarp();
+  for (unsigned i = lane; i < n; i += 32) {
+    const unsigned long long e = q[i];
+    const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
+    rk[i] = (unsigned short)(atomicAdd(&hist[d], 1u | ((unsigned)((e >> EV_LANE_BIT) & 1) << 16)) & 0xFFFFu);
+  }
+  __syncwarp();
+  for (unsigned d = lane; d < WHEEL; d += 32) {
+    const unsigned h = hist[d], cnt = h & 0xFFFFu;
+    if (!cnt) continue;
+    const unsigned b = (unsigned)((t + d) & (WHEEL - 1));
+    while (atomicCAS(&sm.rlock[d], 0, 1) != 0) { }
+    volatile unsigned* rfill = sm.rfill;
+    volatile unsigned* rcap = sm.rcap;
+    volatile unsigned long long* rpos = sm.rpos;
+    if (rfill[d] + cnt > rcap[d]) {
+      if (rfill[d]) file_run(s, b, rpos[d], rfill[d]);
+      const unsigned size = max(region, cnt);
+      rpos[d] = atomicAdd(&s.ctl->ev_head, (unsigned long long)size);
+      rfill[d] = 0;
+      rcap[d] = size;
+    }
+    const unsigned long long base = rpos[d] + rfill[d];
+    rfill[d] = rfill[d] + cnt;
+    __threadfence_block();
+    atomicExch(&sm.rlock[d], 0);
+    hist[d] = (unsigned)(base & s.ev_mask);   // the ring holds at most 2^32 slots
+    atomicAdd(s.bnev + b, cnt);
+    if (h >> 16) atomicAdd(s.bnlane + b, h >> 16);
+  }
+  __syncwarp();
+  for (unsigned i = lane; i < n; i += 32) {
+    const unsigned long long e = q[i];
+    const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
+    st_hint(s.ev + ((hist[d] + (unsigned long long)rk[i]) & s.ev_mask), e & ((1ull << EV_DELAY_SHIFT) - 1),
+            pol_first());
+  }
+  __syncwarp();
+  if (lane == 0) sm.wnp[w] = 0;
+  __syncwarp();
+}
+
+__device__ void ev_push_warp(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t,
+                             unsigned region) {
+  const unsigned m = __ballot_sync(0xFFFFFFFFu, pred);
+  if (m == 0) return;
+  const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  unsigned n = sm.wnp[w];
+  if (n + (unsigned)__popc(m) > WQ) {
+    warp_flush(s, sm, t, region);
+    n = 0;
+  }
+  if (pred) sm.qp[(size_t)w * WQ + n + __popc(m & ((1u << lane) - 1u))] = rec | ((unsigned long long)delay << EV_DELAY_SHIFT);
+  __syncwarp();
+  if (lane == 0) sm.wnp[w] = n + (unsigned)__popc(m);
+  __syncwarp();
+}
+
+// End of a treat phase: after every warp has filed its events, file the open regions.
+__device__ void regions_close(const Dev& s, Smem& sm, long long t) {
+  __syncthreads();
+  for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
+    if (sm.rfill[d]) file_run(s, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d]);
+    sm.rfill[d] = 0;
+    sm.rcap[d] = 0;
+  }
+  __syncthreads();
+}
+#endif
+
 // Counting-sort sm.qp[0, n) by delay and append each delay's events to the
 // block's open region for that delay (opening a new region of `region` slots
 // when it is full).

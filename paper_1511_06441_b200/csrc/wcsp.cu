@@ -139,9 +139,12 @@ cudaError_t set_smem_attrs() {
                  reinterpret_cast<void*>(&k_treat<D>), reinterpret_cast<void*>(&k_wheel_persistent<D>),
                  reinterpret_cast<void*>(&k_wheel_fire<D>), reinterpret_cast<void*>(&k_wheel_treat<D>),
                  reinterpret_cast<void*>(&k_wheel_peer<D>)};
+  const char* co = getenv("WCSP_CARVEOUT");       // A/B runs: shared-memory carveout in percent of L1
   for (void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
+    if (co && (e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(co))) != cudaSuccess)
+      return e;
   }
   return cudaSuccess;
 }

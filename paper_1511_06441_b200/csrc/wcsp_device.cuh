@@ -319,7 +319,8 @@ struct Smem {
   unsigned long long qp[QP_CAP];   // phantom / event staging (wheel: delay in bits 56..63)
   unsigned qa[QA_CAP];             // active-list staging
   union {
-    unsigned wl[WARPS][WIN_VERTS]; // per-warp list of the triggered vertices of its window
+    unsigned short wl[WARPS][WIN_VERTS];   // per-warp list of the triggered vertices of its window
+                                           // (offsets in the window: a small footprint leaves L1 room)
     unsigned short rank[QP_CAP];   // wheel flush: rank of an event within its delay bin
   };
   unsigned hist[WHEEL], hlane[WHEEL], rfill[WHEEL], rcap[WHEEL];
@@ -629,7 +630,7 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
 // (round * gridDim + block) * WARPS + w, clears it and lists its set bits in
 // ascending vertex order (sorted processing: neighbouring Q share sectors).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsigned* list) {
+__device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsigned short* list) {
   // every lane takes 32 / lpw bits of one word (lpw lanes per word), so the serial
   // bit extraction is short and all 32 lanes share it
   const unsigned lane = threadIdx.x & 31u;
@@ -648,9 +649,9 @@ __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsi
   }
   const unsigned total = __shfl_sync(0xFFFFFFFFu, x, 31);
   unsigned pos = x - c;
-  const unsigned vbase = wi * 32u + sub * bpl;
+  const unsigned vbase = (lane / lpw) * 32u + sub * bpl;   // offset in the window
   while (w) {
-    list[pos++] = vbase + (unsigned)(__ffs(w) - 1);
+    list[pos++] = (unsigned short)(vbase + (unsigned)(__ffs(w) - 1));
     w &= w - 1u;
   }
   __syncwarp();
@@ -834,7 +835,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
     const unsigned win = win0 + r * WARPS + warp;
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
-      const unsigned q = b + lane < total ? sm.wl[warp][b + lane] : 0xFFFFFFFFu;
+      const unsigned q = b + lane < total ? win * s.win_words * 32u + sm.wl[warp][b + lane] : 0xFFFFFFFFu;
       treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
     }
     if constexpr (WHEEL_ENGINE) {

@@ -275,7 +275,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   constexpr unsigned CH = FIRE_ITEMS * 32;
   constexpr unsigned MAXD = 512;
   unsigned long long* dpos = reinterpret_cast<unsigned long long*>(&sm.wl[0][0]);   // [MAXD]
-  unsigned* dchunk = &sm.wl[0][0] + 2 * MAXD;                                         // [MAXD + 1] prefix
+  unsigned* dchunk = reinterpret_cast<unsigned*>(dpos + MAXD);                        // [MAXD + 1] prefix
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   unsigned long long arr = 0;
   // Dense cycles: first arrivals near the block's own slab of the grid (its treat windows and one

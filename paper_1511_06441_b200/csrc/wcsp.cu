@@ -242,7 +242,10 @@ wcsp_status alloc_ring(wcsp_handle* h, unsigned long long cap) {
   if (h->ev) cudaFree(h->ev);
   h->ev = nullptr;
   h->ev_cap = 0;
-  cap = std::min(pow2_at_least(cap), 1ull << 32);   // ring slot indices are 32-bit in the treat's filing
+  cap = pow2_at_least(cap);
+#if WCSP_WARP_FLUSH
+  cap = std::min(cap, 1ull << 32);                  // ring slot indices are 32-bit in the warp-level filing
+#endif
   CK(cudaMalloc(&h->ev, cap * sizeof(unsigned long long)));
   h->ev_cap = cap;
   return WCSP_REACHED;

@@ -502,3 +502,25 @@ def test_stamp_wrap_long_run(engine):
     r = wcsp.solve(s, engine=engine, time_mode="unit")
     assert r.key() == oracle.solve_lex(s, 2).key()
     assert r.F1 == n - 1 and r.cycles == n - 1
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("WCSP_TEST_C5") != "1", reason="C5 (1024^3, ~105 GB of HBM, ~6 min): set WCSP_TEST_C5=1")
+def test_C5_full_size_one_gpu():
+    """configs[4] unsliced on one B200: at both M endpoints the oracle's tier-3
+    values (scripts/make_mbind.py, data/mbind.json) are reproduced exactly;
+    at M_bind the run satisfies F2 < M and F1_lex <= F1 <= F1 at F2_min (P5)."""
+    table = json.load(open(os.path.join(os.path.dirname(I.__file__), "data", "mbind.json")))
+    g = table["C5/0"]
+    inst = I.config_face((1024, 1024, 1024), 0, g["M_bind"])
+    with wcsp.Solver(inst, engine="wheel") as s:
+        r = s.solve()
+        assert r.status == wcsp.REACHED and r.F2 < g["M_bind"] and g["F1_lex"] <= r.F1 <= g["F1_at_F2min"]
+        s.set_targets(M=g["F2_lex"] + 1)
+        r_hi = s.solve()
+        assert (r_hi.F1, r_hi.F2) == (g["F1_lex"], g["F2_lex"])
+        s.set_targets(M=g["F2_min"] + 1)
+        r_lo = s.solve()
+        assert (r_lo.F1, r_lo.F2) == (g["F1_at_F2min"], g["F2_min"])
+        s.set_targets(M=g["F2_min"])
+        assert s.solve().status == wcsp.INFEASIBLE

@@ -471,10 +471,59 @@ __device__ Prop wheel_propose(const Dev& s, const View& v, long long* need) {
   return p;
 }
 
+// The same proposal computed by a whole warp (every lane calls it): the scan for the next
+// non-empty bucket and the walk back over the cycles whose events may still be live read
+// 32 slots per step instead of one dependent load after another.
+__device__ Prop wheel_propose_warp(const Dev& s, const View& v, long long* need) {
+  const unsigned lane = threadIdx.x & 31u;
+  Acc* a = &s.ctl->acc[v.c % 3];
+  Ctl* C = s.ctl;
+  const unsigned b = (unsigned)(v.t & (WHEEL - 1));
+  Prop p;
+  {
+    const long long pl = __ldcg((const long long*)&a->pend_lanes);
+    const long long pp = __ldcg((const long long*)&a->pend_phantoms);
+    const long long fired = v.c > 0 ? (long long)__ldcg(s.bnev + b) : 0;
+    const long long fired_l = v.c > 0 ? (long long)__ldcg(s.bnlane + b) : 0;
+    const long long npl = pl - fired_l + (long long)__ldcg(&a->started);
+    const long long npp = pp - (fired - fired_l) + (long long)__ldcg(&a->created);
+    p.bhit = (long long)__ldcg(&a->bhit);
+    p.pending = npl + npp > 0;
+  }
+  unsigned k = 1;
+  if (!s.unit) {
+    k = WHEEL;
+    for (unsigned k0 = 1; k0 < (unsigned)WHEEL; k0 += 32) {
+      const unsigned kk = k0 + lane;
+      const bool nz = kk < (unsigned)WHEEL && __ldcg(s.bnev + ((b + kk) & (WHEEL - 1))) != 0;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, nz);
+      if (m) { k = k0 + (unsigned)(__ffs(m) - 1); break; }
+    }
+  }
+  p.negk = -(long long)k;
+  const unsigned long long head = __ldcg(&C->ev_head);
+  const unsigned lim = min((unsigned)WHEEL, v.c + 1u);   // slots back = 0 .. lim - 1
+  unsigned B = lim;                                      // first back whose cycle's events are all fired
+  for (unsigned b0 = 0; b0 < lim; b0 += 32) {
+    const unsigned back = b0 + lane;
+    const bool done = back < lim &&
+                      __ldcg((const long long*)&C->hist_t[(v.c - back) & (WHEEL - 1)]) + s.f1max <= v.t;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, done);
+    if (m) { B = b0 + (unsigned)(__ffs(m) - 1); break; }
+  }
+  const unsigned long long oldest = B == 0 ? head : __ldcg(&C->hist_head[(v.c - (B - 1)) & (WHEEL - 1)]);
+  *need = 0;
+  p.overflow = 0;
+  if (__ldcg(&C->wheel_overflow)) { p.overflow = 1; *need = -2; }
+  if (head - oldest > s.ev_mask + 1) { p.overflow = 1; *need = (long long)(head - oldest); }
+  return p;
+}
+
 // decide for the wheel (Step 6 + time skipping).  Single device: g = its own
 // proposal; slab engine: g = the max-combined proposals of all slabs.  Reads
 // only state no block writes during decide.
-__device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gext = nullptr) {
+__device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gext = nullptr,
+                             const Prop* lpre = nullptr, long long need_pre = 0) {
   Acc* a = &s.ctl->acc[v.c % 3];
   Ctl* C = s.ctl;
   View nv = v;
@@ -486,8 +535,8 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gex
   const long long new_l = (long long)__ldcg(&a->started);             // lanes started this cycle
   const long long new_p = (long long)__ldcg(&a->created);             // phantoms created this cycle
   const long long npl = pl - fired_l + new_l, npp = pp - (fired - fired_l) + new_p;
-  long long need = 0;
-  const Prop L = wheel_propose(s, v, &need);
+  long long need = need_pre;
+  const Prop L = lpre ? *lpre : wheel_propose(s, v, &need);
   Prop G = L;
   if (gext) {
     G = *gext;
@@ -676,10 +725,14 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_persistent(Dev s) 
       if (!grid_sync(s.ctl, target, sm, &s.ctl->fin[v.c & 1][1][0])) return;
     }
     const View prev = v;
-    if (threadIdx.x == 0) {
-      View nv = v;
-      wheel_decide(s, nv, blockIdx.x == 0);
-      sm.view = nv;
+    if (threadIdx.x < 32) {          // warp 0: the proposal in parallel, then lane 0 decides
+      long long need = 0;
+      const Prop L = wheel_propose_warp(s, v, &need);
+      if (threadIdx.x == 0) {
+        View nv = v;
+        wheel_decide(s, nv, blockIdx.x == 0, nullptr, &L, need);
+        sm.view = nv;
+      }
     }
     __syncthreads();
     v = sm.view;

@@ -334,6 +334,7 @@ struct Smem {
   unsigned short wrank[QP_CAP];
   int rlock[WHEEL];
 #endif
+  unsigned wtot[WARPS];            // treat, shared rounds: triggered vertices per warp window
   unsigned na, np, nspill;
   unsigned bm_lo, bm_words;        // wheel fire, dense cycles: the block's triggered bitmap in qp covers
                                    // vertices [bm_lo, bm_lo + 32 * bm_words)
@@ -658,6 +659,38 @@ __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsi
   return total;
 }
 
+// Shared rounds (WCSP_ROUND_SHARE): the WARPS windows of a round form one list in vertex
+// order that all warps of the block work through together, so a round lasts the mean of its
+// windows' work instead of the max.  window_bits loads and clears one window and returns this
+// lane's share of its bits; window_emit writes them at `base` as offsets in the round.
+__device__ __forceinline__ unsigned window_bits(const Dev& s, unsigned win, unsigned nwin) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned ww = s.win_words, lpw = 32u / ww, bpl = 32u / lpw;
+  const unsigned wi = win * ww + lane / lpw, sub = lane % lpw;
+  unsigned w = win < nwin && wi < s.nwords ? __ldcg(s.tbits + wi) : 0u;
+  __syncwarp();
+  if (sub == 0 && w) s.tbits[wi] = 0u;
+  return (w >> (sub * bpl)) & (bpl == 32u ? 0xFFFFFFFFu : ((1u << bpl) - 1u));
+}
+__device__ __forceinline__ void window_emit(const Dev& s, unsigned bits, unsigned base, unsigned short* list,
+                                            unsigned woff) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned ww = s.win_words, lpw = 32u / ww, bpl = 32u / lpw, sub = lane % lpw;
+  const unsigned cnt = __popc(bits);
+  unsigned x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if ((int)lane >= o) x += y;
+  }
+  unsigned pos = base + x - cnt;
+  const unsigned vbase = woff + (lane / lpw) * 32u + sub * bpl;
+  while (bits) {
+    list[pos++] = (unsigned short)(vbase + (unsigned)(__ffs(bits) - 1));
+    bits &= bits - 1u;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // treat: Steps 4, 5, 8.1 for one triggered vertex q (both engines).
 // WHEEL = false: lanes are residual bytes in res[q]; phantoms go to the pool.
@@ -678,12 +711,15 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #ifndef WCSP_TREAT_EAGER
 #define WCSP_TREAT_EAGER 0         // 1: issue the neighbour loads together with Q's own (measured: no gain on C3)
 #endif
+#ifndef WCSP_ROUND_SHARE
+#define WCSP_ROUND_SHARE 1         // the warps of a block share each treat round's vertices
+#endif
 #ifndef WCSP_WARP_FLUSH
 #define WCSP_WARP_FLUSH 0          // 1: every warp files its own events (no block barriers in the treat);
                                    //    measured on C3: treat +9 %, fire +64 % (interleaved runs) -- off
 #endif
 #ifndef WCSP_FLUSH_LAZY
-#define WCSP_FLUSH_LAZY (QP_CAP / 2)   // > 0: treat flushes its staged events only above this many
+#define WCSP_FLUSH_LAZY (WCSP_QP_CAP / 2)   // > 0: treat flushes its staged events only above this many
 #endif
 __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long long rec, unsigned delay, long long t);
 __device__ void ev_push(const Dev& s, Smem& sm, bool pred, unsigned long long rec, unsigned delay, long long t);
@@ -831,6 +867,35 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
 #endif
     }
   }
+#if WCSP_ROUND_SHARE && WCSP_FLUSH_LAZY > 0 && !WCSP_WARP_FLUSH
+  if constexpr (WHEEL_ENGINE) {
+    unsigned short* flat = &sm.wl[0][0];
+    const unsigned ww = s.win_words;
+    unsigned bits = scan && rounds > 0 ? window_bits(s, win0 + warp, nwin) : 0u;
+    for (unsigned r = 0; scan && r < rounds; ++r) {
+      const unsigned cnt = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(bits));
+      if (lane == 0) sm.wtot[warp] = cnt;
+      __syncthreads();
+      if (sm.np > (unsigned)WCSP_FLUSH_LAZY) ev_flush(s, sm, v.t, v.region, false);   // uniform
+      unsigned base = 0, T = 0;
+#pragma unroll
+      for (unsigned i = 0; i < (unsigned)WARPS; ++i) {
+        const unsigned t = sm.wtot[i];
+        base += i < warp ? t : 0u;
+        T += t;
+      }
+      window_emit(s, bits, base, flat, warp * ww * 32u);
+      __syncthreads();
+      if (r + 1 < rounds) bits = window_bits(s, win0 + (r + 1) * WARPS + warp, nwin);   // next round in flight
+      const unsigned rbase = (win0 + r * WARPS) * ww * 32u;
+      for (unsigned b = warp * 32; b < T; b += WARPS * 32) {
+        const unsigned q = b + lane < T ? rbase + flat[b + lane] : 0xFFFFFFFFu;
+        treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
+      }
+    }
+    scan = false;
+  }
+#endif
   for (unsigned r = 0; scan && r < rounds; ++r) {
     const unsigned win = win0 + r * WARPS + warp;
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;

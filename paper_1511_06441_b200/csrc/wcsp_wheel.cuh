@@ -303,8 +303,8 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
       sm.bm_words = (unsigned)((hi - lo + 31) / 32);
     }
     __syncthreads();
-    unsigned* bm = reinterpret_cast<unsigned*>(sm.qp);
-    for (unsigned i = threadIdx.x; i < sm.bm_words; i += THREADS) bm[i] = 0u;
+    uint4* bm4 = reinterpret_cast<uint4*>(sm.qp);   // 16-byte stores (qp is 16-byte aligned)
+    for (unsigned i = threadIdx.x; i < (sm.bm_words + 3) / 4; i += THREADS) bm4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   for (unsigned d0 = 0; d0 < nd; d0 += MAXD) {
     const unsigned n = min(MAXD, nd - d0);
@@ -410,13 +410,18 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   }
   if (local_bits) {                 // merge the shared-memory bitmap
     __syncthreads();
-    const unsigned* bm = reinterpret_cast<const unsigned*>(sm.qp);
-    const unsigned w0 = sm.bm_lo >> 5;
-    for (unsigned i = threadIdx.x; i < sm.bm_words; i += THREADS) {
-      const unsigned w = bm[i];
-      if (w) {
-        if constexpr (PEER) atom_or_sys(s.tbits + w0 + i, w);   // the neighbours OR into it too
-        else atomicOr(s.tbits + w0 + i, w);
+    const uint4* bm4 = reinterpret_cast<const uint4*>(sm.qp);
+    const unsigned w0 = sm.bm_lo >> 5, nw = sm.bm_words;
+    for (unsigned i = threadIdx.x; i < (nw + 3) / 4; i += THREADS) {
+      const uint4 q4 = bm4[i];
+      const unsigned ws[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned w = ws[k], j = 4 * i + k;
+        if (w && j < nw) {
+          if constexpr (PEER) atom_or_sys(s.tbits + w0 + j, w);   // the neighbours OR into it too
+          else atomicOr(s.tbits + w0 + j, w);
+        }
       }
     }
   }

@@ -428,6 +428,10 @@ def test_full_size_counters_vs_model(key):
         r = wcsp.solve(inst, engine=engine)
         assert list(r.key()) == g["key"]
         assert model_counters(r) == want, (key, engine, r)
+    # the peer-halo slab engine (2 and 4 virtual slabs) gives the same counters at full size
+    for slabs in (2, 4):
+        r = wcsp.solve(inst, engine="wheel", slabs=slabs, halo="peer")
+        assert list(r.key()) == g["key"] and model_counters(r) == want, (key, slabs, r)
 
 
 @pytest.mark.parametrize("halo", ["copy", "peer"])

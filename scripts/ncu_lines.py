@@ -12,7 +12,7 @@ import tempfile
 
 rep, kern, mangled = sys.argv[1:4]
 n = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-so = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1511_06441_b200", "libwcsp.so")
+so = os.environ.get("WCSP_LIB") or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1511_06441_b200", "libwcsp.so")
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
 cubin = os.path.join(tmp, [f for f in os.listdir(tmp) if f.endswith(".cubin")][0])

@@ -203,17 +203,28 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 #ifndef WCSP_L2_HINTS
 #define WCSP_L2_HINTS 1
 #endif
+#ifndef WCSP_POL_PURE
+#define WCSP_POL_PURE 1            // createpolicy as a pure asm (one per kernel after CSE, not one per access)
+#endif
 __device__ __forceinline__ unsigned long long pol_first() {
   unsigned long long p = 0;
 #if WCSP_L2_HINTS
+#if WCSP_POL_PURE
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));   // pure: CSE / hoisting allowed
+#else
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
 #endif
   return p;
 }
 __device__ __forceinline__ unsigned long long pol_last() {
   unsigned long long p = 0;
 #if WCSP_L2_HINTS
+#if WCSP_POL_PURE
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));   // pure: CSE / hoisting allowed
+#else
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
 #endif
   return p;
 }
@@ -240,6 +251,14 @@ __device__ __forceinline__ unsigned atom_max_hint(unsigned* a, unsigned v, unsig
   return old;
 #else
   return atomicMax(a, v);
+#endif
+}
+
+__device__ __forceinline__ void red_max_hint(unsigned* a, unsigned v, unsigned long long pol) {
+#if WCSP_L2_HINTS
+  asm volatile("red.global.max.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+#else
+  atomicMax(a, v);
 #endif
 }
 
@@ -718,6 +737,9 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #define WCSP_WARP_FLUSH 0          // 1: every warp files its own events (no block barriers in the treat);
                                    //    measured on C3: treat +9 %, fire +64 % (interleaved runs) -- off
 #endif
+#ifndef WCSP_TREAT_AGG
+#define WCSP_TREAT_AGG 1           // one warp-scan staging reservation per treat batch (not one per lane direction)
+#endif
 #ifndef WCSP_FLUSH_LAZY
 #define WCSP_FLUSH_LAZY (WCSP_QP_CAP / 2)   // > 0: treat flushes its staged events only above this many
 #endif
@@ -779,6 +801,8 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
   }
   LW neww = 0;
   unsigned fmax = 0;
+  unsigned pm = 0, spm = 0;          // WCSP_TREAT_AGG: the lanes whose edge passed (bit j), and those
+                                     // whose destination holds a sentinel temp (target, ghost: bit 50)
 #pragma unroll
   for (int j = 0; j < 2 * D; ++j) {
     const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
@@ -793,13 +817,19 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     lanes_started += pass && inactive;                            // activate, time restored to f1 (:192)
     if constexpr (WHEEL_ENGINE) {
       if (pass && inactive) fmax = max(fmax, f1j);
+#if WCSP_TREAT_AGG && !WCSP_WARP_FLUSH
+      pm |= (pass ? 1u : 0u) << j;
+      spm |= ((rtw >> 16) == 0xFFFFu ? 1u : 0u) << j;
+#else
       const unsigned long long rec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
                                      ((unsigned long long)(unsigned)c << PH_CAND) |
-                                     ((unsigned long long)(inactive ? 1u : 0u) << 49);
+                                     ((unsigned long long)(inactive ? 1u : 0u) << 49) |
+                                     ((unsigned long long)((rtw >> 16) == 0xFFFFu ? 1u : 0u) << 50);
 #if WCSP_WARP_FLUSH
       ev_push_warp(s, sm, pass, rec, f1j, v.t, v.region);
 #else
       ev_push(s, sm, pass, rec, f1j, v.t);
+#endif
 #endif
     } else {
       if (pass) dmin = min(dmin, f1j);
@@ -810,6 +840,39 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       qpush<unsigned long long>(sm.qp, QP_CAP, &sm.np, ph, prec, &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
     }
   }
+#if WCSP_TREAT_AGG && !WCSP_WARP_FLUSH
+  if constexpr (WHEEL_ENGINE) {
+    // one staging reservation per warp for all its vertices' events (an exclusive scan of the
+    // per-thread counts) instead of one ballot + shared atomic per lane direction
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned cnt = __popc(pm);
+    unsigned x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if ((int)lane >= o) x += y;
+    }
+    const unsigned tot = __shfl_sync(0xFFFFFFFFu, x, 31);
+    if (tot) {                       // warp-uniform
+      unsigned base = 0;
+      if (lane == 31) base = atomicAdd(&sm.np, tot);
+      base = __shfl_sync(0xFFFFFFFFu, base, 31);
+      unsigned idx = base + x - cnt;
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j) {
+        if ((pm >> j) & 1u) {
+          const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
+          const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
+          const unsigned long long rec = (unsigned long long)q | ((unsigned long long)j << PH_LANE) |
+                                         ((unsigned long long)(unsigned)(lstar - (int)f2j) << PH_CAND) |
+                                         ((unsigned long long)(inactive ? 1u : 0u) << 49) |
+                                         ((unsigned long long)((spm >> j) & 1u) << 50);
+          ev_stage(s, sm, idx++, rec, f1j, v.t);
+        }
+      }
+    }
+  }
+#endif
   if (inactive) {                                                 // Step 8.1
     relabels += 1;
     if constexpr (WHEEL_ENGINE) {

@@ -27,6 +27,12 @@
 namespace wcspk {
 
 constexpr int EV_LANE_BIT = 49;
+constexpr int EV_SPECIAL_BIT = 50;        // the destination's temp is a sentinel (target / ghost): the fire
+                                          // needs the atomic's old value for it
+#ifndef WCSP_FIRE_RED
+#define WCSP_FIRE_RED 0                   // dense single-device fires: ordinary arrivals as fire-and-forget
+                                          // reductions (red.max) and an unconditional bitmap bit
+#endif
 constexpr int EV_DELAY_SHIFT = 56;
 constexpr unsigned MAINT_PERIOD_T = 1u << 15;
 #ifndef WCSP_FIRE_ITEMS
@@ -283,6 +289,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   // shared-memory bitmap (the treat staging is free during the fire), merged into the global
   // bitmap with one atomicOr per word at the end; sparse cycles list them (see arrive_post).
   const bool local_bits = (PEER || !s.slab) && !v.lmode;
+  const bool redmode = local_bits && !PEER;
   if (local_bits) {
     if (threadIdx.x == 0) {
       const unsigned long long ww = s.win_words, nwin = (s.nwords + ww - 1) / ww;
@@ -394,6 +401,21 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
           old[it] = arrive_atomic<PEER>(s, v, valid && !skip[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));
           if (skip[it]) old[it] = v.stamp << 16;   // as if a later arrival of this cycle: nothing to do
           continue;
+        }
+#endif
+#if WCSP_FIRE_RED
+        if constexpr (!PEER) {
+          // No first-arrival test needed here: the bit of D is set on every arrival (same set
+          // of bits), so only sentinel destinations (targets, ghosts) need the old value.
+          if (redmode && valid && !((e[it] >> EV_SPECIAL_BIT) & 1)) {
+            const unsigned dst = src + s.off[ln];
+            red_max_hint(tmp_ptr(s.sw, dst), (v.stamp << 16) | (unsigned)((e[it] >> PH_CAND) & 0xFFFFu), pol_last());
+            const unsigned r = dst - sm.bm_lo;
+            if (r < sm.bm_words * 32u) atomicOr(reinterpret_cast<unsigned*>(sm.qp) + (r >> 5), 1u << (r & 31u));
+            else atomicOr(s.tbits + (dst >> 5), 1u << (dst & 31u));
+            old[it] = v.stamp << 16;       // as if a later arrival of this cycle: arrive_post does nothing
+            continue;
+          }
         }
 #endif
         old[it] = arrive_atomic<PEER>(s, v, valid, src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));

@@ -30,7 +30,7 @@ constexpr int EV_LANE_BIT = 49;
 constexpr int EV_SPECIAL_BIT = 50;        // the destination's temp is a sentinel (target / ghost): the fire
                                           // needs the atomic's old value for it
 #ifndef WCSP_FIRE_RED
-#define WCSP_FIRE_RED 0                   // dense single-device fires: ordinary arrivals as fire-and-forget
+#define WCSP_FIRE_RED 1                   // dense single-device fires: ordinary arrivals as fire-and-forget
                                           // reductions (red.max) and an unconditional bitmap bit
 #endif
 constexpr int EV_DELAY_SHIFT = 56;

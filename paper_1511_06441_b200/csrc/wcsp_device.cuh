@@ -485,6 +485,9 @@ __device__ __forceinline__ unsigned atom_max_sys(unsigned* a, unsigned v) {
   asm volatile("atom.relaxed.sys.global.max.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ void red_max_sys(unsigned* a, unsigned v) {
+  asm volatile("red.relaxed.sys.global.max.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ void atom_or_sys(unsigned* a, unsigned v) {
   asm volatile("red.relaxed.sys.global.or.b32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
@@ -691,6 +694,22 @@ __device__ __forceinline__ unsigned window_bits(const Dev& s, unsigned win, unsi
   if (sub == 0 && w) s.tbits[wi] = 0u;
   return (w >> (sub * bpl)) & (bpl == 32u ? 0xFFFFFFFFu : ((1u << bpl) - 1u));
 }
+// The same in two steps, so the load of the next round's window can be in flight while the
+// current round is treated: window_load issues it; window_use (at the next round) clears the
+// word and returns this lane's share of its bits.
+__device__ __forceinline__ unsigned window_load(const Dev& s, unsigned win, unsigned nwin) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned ww = s.win_words, lpw = 32u / ww;
+  const unsigned wi = win * ww + lane / lpw;
+  return win < nwin && wi < s.nwords ? __ldcg(s.tbits + wi) : 0u;
+}
+__device__ __forceinline__ unsigned window_use(const Dev& s, unsigned win, unsigned w) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned ww = s.win_words, lpw = 32u / ww, bpl = 32u / lpw;
+  const unsigned wi = win * ww + lane / lpw, sub = lane % lpw;
+  if (sub == 0 && w) s.tbits[wi] = 0u;
+  return (w >> (sub * bpl)) & (bpl == 32u ? 0xFFFFFFFFu : ((1u << bpl) - 1u));
+}
 __device__ __forceinline__ void window_emit(const Dev& s, unsigned bits, unsigned base, unsigned short* list,
                                             unsigned woff) {
   const unsigned lane = threadIdx.x & 31u;
@@ -736,6 +755,9 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #ifndef WCSP_WARP_FLUSH
 #define WCSP_WARP_FLUSH 0          // 1: every warp files its own events (no block barriers in the treat);
                                    //    measured on C3: treat +9 %, fire +64 % (interleaved runs) -- off
+#endif
+#ifndef WCSP_WIN_PREFETCH
+#define WCSP_WIN_PREFETCH 0        // 1: the next round's bitmap words load while this round is treated (no gain; off)
 #endif
 #ifndef WCSP_TREAT_AGG
 #define WCSP_TREAT_AGG 1           // one warp-scan staging reservation per treat batch (not one per lane direction)
@@ -934,8 +956,15 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   if constexpr (WHEEL_ENGINE) {
     unsigned short* flat = &sm.wl[0][0];
     const unsigned ww = s.win_words;
+#if WCSP_WIN_PREFETCH
+    unsigned raw = scan && rounds > 0 ? window_load(s, win0 + warp, nwin) : 0u;
+#else
     unsigned bits = scan && rounds > 0 ? window_bits(s, win0 + warp, nwin) : 0u;
+#endif
     for (unsigned r = 0; scan && r < rounds; ++r) {
+#if WCSP_WIN_PREFETCH
+      const unsigned bits = window_use(s, win0 + r * WARPS + warp, raw);
+#endif
       const unsigned cnt = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(bits));
       if (lane == 0) sm.wtot[warp] = cnt;
       __syncthreads();
@@ -949,7 +978,11 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
       }
       window_emit(s, bits, base, flat, warp * ww * 32u);
       __syncthreads();
-      if (r + 1 < rounds) bits = window_bits(s, win0 + (r + 1) * WARPS + warp, nwin);   // next round in flight
+#if WCSP_WIN_PREFETCH
+      if (r + 1 < rounds) raw = window_load(s, win0 + (r + 1) * WARPS + warp, nwin);   // next round in flight
+#else
+      if (r + 1 < rounds) bits = window_bits(s, win0 + (r + 1) * WARPS + warp, nwin);
+#endif
       const unsigned rbase = (win0 + r * WARPS) * ww * 32u;
       for (unsigned b = warp * 32; b < T; b += WARPS * 32) {
         const unsigned q = b + lane < T ? rbase + flat[b + lane] : 0xFFFFFFFFu;

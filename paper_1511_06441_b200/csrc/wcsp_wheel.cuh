@@ -33,14 +33,16 @@ constexpr int EV_SPECIAL_BIT = 50;        // the destination's temp is a sentine
 #define WCSP_FIRE_RED 1                   // dense single-device fires: ordinary arrivals as fire-and-forget
                                           // reductions (red.max) and an unconditional bitmap bit
 #endif
+#ifndef WCSP_FIRE_RED_PEER
+#define WCSP_FIRE_RED_PEER 1              // ... and in the peer-halo engine (system-scope red.max)
+#endif
 constexpr int EV_DELAY_SHIFT = 56;
 constexpr unsigned MAINT_PERIOD_T = 1u << 15;
 #ifndef WCSP_FIRE_ITEMS
 #define WCSP_FIRE_ITEMS 8
 #endif
-#ifndef WCSP_FIRE_PRECHECK
-#define WCSP_FIRE_PRECHECK 0              // 1: skip atomics an L1 copy of the state word shows to be no-ops
-                                          //    (measured: treat -6 %, fire +35 % on C3 -- off)
+#ifndef WCSP_FIRE_PF
+#define WCSP_FIRE_PF 0                    // 1: chunk c + 1's events load during chunk c (C2 -2 %, C3 +0.5 %: spills; off)
 #endif
 #ifndef WCSP_MINB
 #define WCSP_MINB 3                       // resident blocks per SM the cycle kernels are compiled for
@@ -289,7 +291,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   // shared-memory bitmap (the treat staging is free during the fire), merged into the global
   // bitmap with one atomicOr per word at the end; sparse cycles list them (see arrive_post).
   const bool local_bits = (PEER || !s.slab) && !v.lmode;
-  const bool redmode = local_bits && !PEER;
+  const bool redmode = local_bits;
   if (local_bits) {
     if (threadIdx.x == 0) {
       const unsigned long long ww = s.win_words, nwin = (s.nwords + ww - 1) / ww;
@@ -353,58 +355,51 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
       }
       di = lo;
     }
-    for (unsigned c = c_lo; c < c_hi; ++c) {
+    // chunk c's events: descriptor di (advanced monotonically), FIRE_ITEMS per lane
+    auto load_chunk = [&](unsigned c, unsigned long long (&ev)[FIRE_ITEMS]) {
       while (dchunk[di + 1] <= c) ++di;
       const unsigned long long dsc = dpos[di];
       const unsigned long long pos = dsc >> 24;
       const unsigned cnt = (unsigned)(dsc & 0xFFFFFFu);
       const unsigned base = (c - dchunk[di]) * CH;
-      unsigned long long e[FIRE_ITEMS];
 #pragma unroll
       for (int it = 0; it < FIRE_ITEMS; ++it) {
         const unsigned i = base + it * 32 + lane;
-        e[it] = i < cnt ? ld_hint(s.ev + ((pos + i) & s.ev_mask), pol_first()) : ~0ull;
+        ev[it] = i < cnt ? ld_hint(s.ev + ((pos + i) & s.ev_mask), pol_first()) : ~0ull;
       }
-      unsigned old[FIRE_ITEMS];
-#if WCSP_FIRE_PRECHECK
-      // An arrival that cannot change temp(D) needs no atomic: labels only grow and temps only
-      // grow within a cycle, so if an L1 copy of D's state word (possibly stale, never too
-      // high) already holds L(D) >= cand, or a temp of this cycle >= cand, the atomic would
-      // be a no-op (and D's first arrival has happened or cannot trigger it).  Sentinel temps
-      // (targets, removed, ghosts) are never skipped on the temp rule; removed labels skip.
-      bool skip[FIRE_ITEMS];
-      if constexpr (!PEER) {
-        unsigned long long w[FIRE_ITEMS];
-#pragma unroll
-        for (int it = 0; it < FIRE_ITEMS; ++it) {
-          const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
-          const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
-          w[it] = e[it] != ~0ull ? s.sw[src + s.off[ln]] : 0ull;
-        }
-#pragma unroll
-        for (int it = 0; it < FIRE_ITEMS; ++it) {
-          const unsigned cand = (unsigned)(e[it] >> PH_CAND) & 0xFFFFu;
-          const unsigned tw = (unsigned)(w[it] >> 32);
-          skip[it] = e[it] != ~0ull && (((unsigned)w[it] & 0xFFFFu) >= cand ||
-                                        ((tw >> 16) == v.stamp && (tw & 0xFFFFu) >= cand));
-        }
-      }
+    };
+    unsigned long long e[FIRE_ITEMS];
+    if (c_lo < c_hi) load_chunk(c_lo, e);
+    for (unsigned c = c_lo; c < c_hi; ++c) {
+#if WCSP_FIRE_PF
+      unsigned long long en[FIRE_ITEMS];   // the next chunk's events load while this one fires
+      if (c + 1 < c_hi) load_chunk(c + 1, en);
 #endif
+      unsigned old[FIRE_ITEMS];
 #pragma unroll
       for (int it = 0; it < FIRE_ITEMS; ++it) {   // put every atomic in flight before using a result
         const bool valid = e[it] != ~0ull;
         arr += valid;
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
-#if WCSP_FIRE_PRECHECK
-        if constexpr (!PEER) {
-          old[it] = arrive_atomic<PEER>(s, v, valid && !skip[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));
-          if (skip[it]) old[it] = v.stamp << 16;   // as if a later arrival of this cycle: nothing to do
-          continue;
-        }
-#endif
 #if WCSP_FIRE_RED
-        if constexpr (!PEER) {
+        if constexpr (PEER) {
+#if WCSP_FIRE_RED_PEER
+          // the same with system-scope reductions (a neighbour's words may live on another GPU)
+          if (redmode && valid && !((e[it] >> EV_SPECIAL_BIT) & 1)) {
+            const unsigned dst = src + s.off[ln];
+            const Loc L = locate<true>(s, dst);
+            red_max_sys(tmp_ptr(L.sw, L.idx), (v.stamp << 16) | (unsigned)((e[it] >> PH_CAND) & 0xFFFFu));
+            const unsigned r = dst - sm.bm_lo;
+            if (L.sw == s.sw && r < sm.bm_words * 32u)
+              atomicOr(reinterpret_cast<unsigned*>(sm.qp) + (r >> 5), 1u << (r & 31u));
+            else
+              atom_or_sys(L.tb + (L.idx >> 5), 1u << (L.idx & 31u));
+            old[it] = v.stamp << 16;
+            continue;
+          }
+#endif
+        } else {
           // No first-arrival test needed here: the bit of D is set on every arrival (same set
           // of bits), so only sentinel destinations (targets, ghosts) need the old value.
           if (redmode && valid && !((e[it] >> EV_SPECIAL_BIT) & 1)) {
@@ -428,6 +423,12 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         arrive_post<PEER, true>(s, v, acc, old[it], src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu),
                                 src + s.goff, via, local_bits || (!s.slab && v.lmode) ? &sm : nullptr);
       }
+#if WCSP_FIRE_PF
+#pragma unroll
+      for (int it = 0; it < FIRE_ITEMS; ++it) e[it] = en[it];
+#else
+      if (c + 1 < c_hi) load_chunk(c + 1, e);
+#endif
     }
   }
   if (local_bits) {                 // merge the shared-memory bitmap

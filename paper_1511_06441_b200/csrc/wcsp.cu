@@ -83,6 +83,7 @@ struct wcsp_handle {
   unsigned long long* d_cnt = nullptr;               // validation counters
   long long M = 0;
   int nsm = 0, grid = 0;
+  bool big = false;                                  // wheel: the 4-blocks-per-SM cycle kernel
   cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
   long long last_cycles = 0;
   long long launches = 0;
@@ -120,23 +121,26 @@ namespace {
 size_t lane_bytes(int d) { return d <= 2 ? 4 : 8; }
 
 template <int D>
-void* cycle_fn(int engine) {
+void* cycle_fn(int engine, bool big) {
   switch (engine) {
     case WCSP_ENGINE_PERSISTENT: return reinterpret_cast<void*>(&k_persistent<D>);
     case WCSP_ENGINE_STEPPED: return reinterpret_cast<void*>(&k_sweep<D>);
-    case WCSP_ENGINE_WHEEL: return reinterpret_cast<void*>(&k_wheel_persistent<D>);
+    case WCSP_ENGINE_WHEEL: return big ? reinterpret_cast<void*>(&k_wheel_persistent<D, 4>)
+                                       : reinterpret_cast<void*>(&k_wheel_persistent<D, 3>);
     default: return reinterpret_cast<void*>(&k_wheel_treat<D>);
   }
 }
-void* cycle_fn_d(int d, int engine) {
-  return d == 1 ? cycle_fn<1>(engine) : d == 2 ? cycle_fn<2>(engine) : d == 3 ? cycle_fn<3>(engine) : cycle_fn<4>(engine);
+void* cycle_fn_d(int d, int engine, bool big) {
+  return d == 1 ? cycle_fn<1>(engine, big) : d == 2 ? cycle_fn<2>(engine, big) : d == 3 ? cycle_fn<3>(engine, big)
+                                                                                 : cycle_fn<4>(engine, big);
 }
 
 template <int D>
 cudaError_t set_smem_attrs() {
   const int bytes = (int)sizeof(Smem);
   void* fns[] = {reinterpret_cast<void*>(&k_persistent<D>), reinterpret_cast<void*>(&k_sweep<D>),
-                 reinterpret_cast<void*>(&k_treat<D>), reinterpret_cast<void*>(&k_wheel_persistent<D>),
+                 reinterpret_cast<void*>(&k_treat<D>), reinterpret_cast<void*>(&k_wheel_persistent<D, 3>),
+                 reinterpret_cast<void*>(&k_wheel_persistent<D, 4>),
                  reinterpret_cast<void*>(&k_wheel_fire<D>), reinterpret_cast<void*>(&k_wheel_treat<D>),
                  reinterpret_cast<void*>(&k_wheel_peer<D>)};
   const char* co = getenv("WCSP_CARVEOUT");       // A/B runs: shared-memory carveout in percent of L1
@@ -435,7 +439,7 @@ wcsp_status launch_init(wcsp_handle* h) {
 wcsp_status run_persistent(wcsp_handle* h) {
   Dev s = make_dev(h);
   void* args[] = {&s};
-  CK(cudaLaunchCooperativeKernel(cycle_fn_d(h->d, h->opt.engine), dim3(h->grid), dim3(THREADS), args, sizeof(Smem),
+  CK(cudaLaunchCooperativeKernel(cycle_fn_d(h->d, h->opt.engine, h->big), dim3(h->grid), dim3(THREADS), args, sizeof(Smem),
                                  h->stream));
   h->launches += 1;
   return WCSP_REACHED;
@@ -610,10 +614,17 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
     case 3: CKC(set_smem_attrs<3>()); break;
     default: CKC(set_smem_attrs<4>()); break;
   }
+  // Persistent wheel engine: the build for 4 resident blocks per SM (64 registers) on 3-D and
+  // higher grids of at least 2^21 vertices (thick fronts: C3 157.8 -> 137.3 ms), the one for 3 (80
+  // registers) otherwise, where cycles are short or fronts thin and the grid barriers dominate
+  // (C2 1024^2, C4 fractal: 24.6 vs 31 ms).
+  const char* bps = getenv("WCSP_BLOCKS_PER_SM");                   // A/B runs
+  h->big = opt.engine == WCSP_ENGINE_WHEEL && (bps ? atoi(bps) >= 4 : p->d >= 3 && N >= (1ull << 21));
   int per_sm = 0;
-  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_fn_d(p->d, opt.engine), THREADS, sizeof(Smem)));
+  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_fn_d(p->d, opt.engine, h->big), THREADS,
+                                                    sizeof(Smem)));
   if (per_sm < 1) CKH(fail(WCSP_ECUDA, "cycle kernel cannot be resident"));
-  if (const char* e = getenv("WCSP_BLOCKS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));   // A/B runs
+  if (bps) per_sm = std::max(1, std::min(per_sm, atoi(bps)));
   h->grid = per_sm * h->nsm;
   const size_t fb = (size_t)h->d * N;
   CKC(cudaMalloc(&h->d_f1, fb));

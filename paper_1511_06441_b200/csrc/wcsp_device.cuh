@@ -113,6 +113,8 @@ struct Ctl {
   unsigned long long ybest;        // (src << 1 | via) of the best arrival at X seen by this slab
   unsigned n_stair, pad3_;         // staircase steps recorded
   long long stair_q;               // best target quality so far
+  alignas(128) unsigned long long grel;   // grid barrier: the last block to arrive releases this target
+  unsigned long long pad4_[15];           // (its own 128-byte line: pollers do not slow the arrivals)
 };
 
 struct TraceRec {
@@ -657,8 +659,8 @@ __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsi
   // every lane takes 32 / lpw bits of one word (lpw lanes per word), so the serial
   // bit extraction is short and all 32 lanes share it
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned ww = s.win_words, lpw = 32u / ww, bpl = 32u / lpw;
-  const unsigned wi = win * ww + lane / lpw, sub = lane % lpw;
+  const unsigned ww = s.win_words, lg = __ffs(ww) - 1u, bpl = ww;   // ww: a power of two (no divisions)
+  const unsigned wi = win * ww + (lane >> (5u - lg)), sub = lane & ((32u >> lg) - 1u);
   unsigned w = wi < s.nwords ? __ldcg(s.tbits + wi) : 0u;
   __syncwarp();
   if (sub == 0 && w) s.tbits[wi] = 0u;
@@ -672,7 +674,7 @@ __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsi
   }
   const unsigned total = __shfl_sync(0xFFFFFFFFu, x, 31);
   unsigned pos = x - c;
-  const unsigned vbase = (lane / lpw) * 32u + sub * bpl;   // offset in the window
+  const unsigned vbase = (lane >> (5u - lg)) * 32u + sub * bpl;   // offset in the window
   while (w) {
     list[pos++] = (unsigned short)(vbase + (unsigned)(__ffs(w) - 1));
     w &= w - 1u;
@@ -687,8 +689,8 @@ __device__ __forceinline__ unsigned window_take(const Dev& s, unsigned win, unsi
 // lane's share of its bits; window_emit writes them at `base` as offsets in the round.
 __device__ __forceinline__ unsigned window_bits(const Dev& s, unsigned win, unsigned nwin) {
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned ww = s.win_words, lpw = 32u / ww, bpl = 32u / lpw;
-  const unsigned wi = win * ww + lane / lpw, sub = lane % lpw;
+  const unsigned ww = s.win_words, lg = __ffs(ww) - 1u, bpl = ww;   // ww: a power of two (no divisions)
+  const unsigned wi = win * ww + (lane >> (5u - lg)), sub = lane & ((32u >> lg) - 1u);
   unsigned w = win < nwin && wi < s.nwords ? __ldcg(s.tbits + wi) : 0u;
   __syncwarp();
   if (sub == 0 && w) s.tbits[wi] = 0u;
@@ -699,21 +701,21 @@ __device__ __forceinline__ unsigned window_bits(const Dev& s, unsigned win, unsi
 // word and returns this lane's share of its bits.
 __device__ __forceinline__ unsigned window_load(const Dev& s, unsigned win, unsigned nwin) {
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned ww = s.win_words, lpw = 32u / ww;
-  const unsigned wi = win * ww + lane / lpw;
+  const unsigned ww = s.win_words, lg = __ffs(ww) - 1u;
+  const unsigned wi = win * ww + (lane >> (5u - lg));
   return win < nwin && wi < s.nwords ? __ldcg(s.tbits + wi) : 0u;
 }
 __device__ __forceinline__ unsigned window_use(const Dev& s, unsigned win, unsigned w) {
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned ww = s.win_words, lpw = 32u / ww, bpl = 32u / lpw;
-  const unsigned wi = win * ww + lane / lpw, sub = lane % lpw;
+  const unsigned ww = s.win_words, lg = __ffs(ww) - 1u, bpl = ww;   // ww: a power of two (no divisions)
+  const unsigned wi = win * ww + (lane >> (5u - lg)), sub = lane & ((32u >> lg) - 1u);
   if (sub == 0 && w) s.tbits[wi] = 0u;
   return (w >> (sub * bpl)) & (bpl == 32u ? 0xFFFFFFFFu : ((1u << bpl) - 1u));
 }
 __device__ __forceinline__ void window_emit(const Dev& s, unsigned bits, unsigned base, unsigned short* list,
                                             unsigned woff) {
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned ww = s.win_words, lpw = 32u / ww, bpl = 32u / lpw, sub = lane % lpw;
+  const unsigned ww = s.win_words, lg = __ffs(ww) - 1u, bpl = ww, sub = lane & ((32u >> lg) - 1u);
   const unsigned cnt = __popc(bits);
   unsigned x = cnt;
 #pragma unroll
@@ -722,7 +724,7 @@ __device__ __forceinline__ void window_emit(const Dev& s, unsigned bits, unsigne
     if ((int)lane >= o) x += y;
   }
   unsigned pos = base + x - cnt;
-  const unsigned vbase = woff + (lane / lpw) * 32u + sub * bpl;
+  const unsigned vbase = woff + (lane >> (5u - lg)) * 32u + sub * bpl;
   while (bits) {
     list[pos++] = (unsigned short)(vbase + (unsigned)(__ffs(bits) - 1));
     bits &= bits - 1u;
@@ -758,6 +760,9 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #endif
 #ifndef WCSP_WIN_PREFETCH
 #define WCSP_WIN_PREFETCH 0        // 1: the next round's bitmap words load while this round is treated (no gain; off)
+#endif
+#ifndef WCSP_STAGE_BITLOOP
+#define WCSP_STAGE_BITLOOP 0       // 1: stage a vertex's events in a loop over its passed directions
 #endif
 #ifndef WCSP_TREAT_AGG
 #define WCSP_TREAT_AGG 1           // one warp-scan staging reservation per treat batch (not one per lane direction)
@@ -880,6 +885,19 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       if (lane == 31) base = atomicAdd(&sm.np, tot);
       base = __shfl_sync(0xFFFFFFFFu, base, 31);
       unsigned idx = base + x - cnt;
+#if WCSP_STAGE_BITLOOP
+      // only the passed directions (popc(pm) iterations, not 2d predicated ones)
+      const unsigned long long rc = (unsigned long long)q | ((unsigned long long)(inactive ? 1u : 0u) << 49);
+      for (unsigned m = pm; m; m &= m - 1u) {
+        const unsigned j = (unsigned)__ffs(m) - 1u;
+        const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
+        const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
+        ev_stage(s, sm, idx++,
+                 rc | ((unsigned long long)j << PH_LANE) | ((unsigned long long)(unsigned)(lstar - (int)f2j) << PH_CAND) |
+                     ((unsigned long long)((spm >> j) & 1u) << 50),
+                 f1j, v.t);
+      }
+#else
 #pragma unroll
       for (int j = 0; j < 2 * D; ++j) {
         if ((pm >> j) & 1u) {
@@ -892,6 +910,7 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
           ev_stage(s, sm, idx++, rec, f1j, v.t);
         }
       }
+#endif
     }
   }
 #endif
@@ -1113,6 +1132,12 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // BARRIER_TIMEOUT_NS sets ctl->abort; every waiting block then gives up).
 constexpr unsigned long long BARRIER_TIMEOUT_NS = 20ull * 1000000000ull;
 
+#ifndef WCSP_BAR_RELEASE
+#define WCSP_BAR_RELEASE 0         // 1: the last arriver releases a flag on its own line (measured: C2 +8 %; off)
+#endif
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long x) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
 __device__ __forceinline__ bool grid_sync(Ctl* ctl, unsigned long long target, Smem& sm,
                                           unsigned long long* fin = nullptr) {
   __syncthreads();
@@ -1123,10 +1148,20 @@ __device__ __forceinline__ bool grid_sync(Ctl* ctl, unsigned long long target, S
       atomicAdd(fin + 1, busy);
     }
     __threadfence();
+#if WCSP_BAR_RELEASE
+    // arrivals count on ctl->bar; the last one publishes the release on a line of its own
+    if (atomicAdd(&ctl->bar, 1ull) == target - 1) {
+      __threadfence();
+      st_release_gpu(&ctl->grel, target);
+    }
+    unsigned long long* const poll = &ctl->grel;
+#else
     atomicAdd(&ctl->bar, 1ull);
+    unsigned long long* const poll = &ctl->bar;
+#endif
     const unsigned long long t0 = globaltimer_ns();
     unsigned ok = 1;
-    while (ld_acquire(&ctl->bar) < target) {
+    while (ld_acquire(poll) < target) {
       __nanosleep(32);
       if (*(volatile unsigned*)&ctl->abort) { ok = 0; break; }
       if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&ctl->abort, 1u); ok = 0; break; }

@@ -725,8 +725,11 @@ __device__ __forceinline__ bool needs_maint(const View& prev, const View& nv) {
          (nv.stamp == 1u || (nv.t / MAINT_PERIOD_T) != (prev.t / MAINT_PERIOD_T));
 }
 
-template <int D>
-__global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_persistent(Dev s) {
+// MINB: resident blocks per SM the kernel is compiled for.  4 (64 registers) wins on big grids
+// (C3 157.8 -> 135.6 ms: more warps hide the treat's gather latency), 3 (80 registers) on thin or
+// small ones (C2, C4: fewer blocks in every grid barrier, no spills); the host picks by grid size.
+template <int D, int MINB = WCSP_MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_wheel_persistent(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
   View v;
@@ -739,7 +742,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_persistent(Dev s) 
       if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
       wheel_fire<D>(s, v, sm);
       target += G;
-      if (!grid_sync(s.ctl, target, sm, &s.ctl->fin[v.c & 1][0][0])) return;
+      if (!grid_sync(s.ctl, target, sm, s.trace_cap > 0 ? &s.ctl->fin[v.c & 1][0][0] : nullptr)) return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
     if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
@@ -750,7 +753,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_persistent(Dev s) 
       if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
       phase_treat<D, true>(s, v, sm);
       target += G;
-      if (!grid_sync(s.ctl, target, sm, &s.ctl->fin[v.c & 1][1][0])) return;
+      if (!grid_sync(s.ctl, target, sm, s.trace_cap > 0 ? &s.ctl->fin[v.c & 1][1][0] : nullptr)) return;
     }
     const View prev = v;
     if (threadIdx.x < 32) {          // warp 0: the proposal in parallel, then lane 0 decides
@@ -836,9 +839,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void red_add_release_sys(unsigned long long* p, unsigned long long x) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
 }
-__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long x) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
-}
 
 // propose: the leader, once every block of its slab has arrived (the slab's treat is
 // complete), writes the slab's proposal for the cycle decision before joining the other
@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_peer(const __grid_
       if (leader && threadIdx.x == 0) wheel_cycle_start(s, v);
       if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
       wheel_fire<D, true>(s, v, sm);
-      if (!peer_sync(s, sm, ++epoch, &s.ctl->fin[v.c & 1][0][0])) return;
+      if (!peer_sync(s, sm, ++epoch, s.trace_cap > 0 ? &s.ctl->fin[v.c & 1][0][0] : nullptr)) return;
     }
     if (leader && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
     if (threadIdx.x == 0) {          // a target reached in any slab ends the run (1°)
@@ -928,7 +928,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_peer(const __grid_
       phase_treat<D, true, true>(s, v, sm);
     }
     // end of the treat + every slab's proposal for the decision, in one barrier
-    if (!peer_sync(s, sm, ++epoch, bhit ? nullptr : &s.ctl->fin[v.c & 1][1][0], &v)) return;
+    if (!peer_sync(s, sm, ++epoch, bhit || s.trace_cap <= 0 ? nullptr : &s.ctl->fin[v.c & 1][1][0], &v)) return;
     const View prev = v;
     if (threadIdx.x == 0) {          // every slab takes the same decision from the combined proposal
       Prop G{0, -(long long)WHEEL, 0, 0};

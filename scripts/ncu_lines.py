@@ -1,6 +1,8 @@
 """Warp-stall samples of one kernel in an ncu report, aggregated per CUDA source line
 (SASS offsets mapped to lines with nvdisasm -g on the cubin of the same build).
-usage: ncu_lines.py REPORT KERNEL_REGEX MANGLED_NAME [N]"""
+usage: ncu_lines.py REPORT KERNEL_REGEX MANGLED_NAME [N]
+NCU_COL="Instructions Executed" aggregates executed warp instructions instead of stall samples;
+WCSP_LIB names the build the report was captured with."""
 import csv
 import collections
 import io
@@ -33,7 +35,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"reg
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = next(r for r in rows if r and r[0] == "Address")
-i_s = hdr.index("Warp Stall Sampling (All Samples)")
+i_s = hdr.index(os.environ.get("NCU_COL", "Warp Stall Sampling (All Samples)"))
 items = [(int(r[0], 16), int(r[i_s])) for r in rows if len(r) == len(hdr) and r[0].startswith("0x") and r[i_s].isdigit()]
 base = min(a for a, _ in items)
 agg = collections.Counter()

@@ -142,7 +142,7 @@ cudaError_t set_smem_attrs() {
                  reinterpret_cast<void*>(&k_treat<D>), reinterpret_cast<void*>(&k_wheel_persistent<D, 3>),
                  reinterpret_cast<void*>(&k_wheel_persistent<D, 4>),
                  reinterpret_cast<void*>(&k_wheel_fire<D>), reinterpret_cast<void*>(&k_wheel_treat<D>),
-                 reinterpret_cast<void*>(&k_wheel_peer<D>)};
+                 reinterpret_cast<void*>(&k_wheel_peer<D, 3>), reinterpret_cast<void*>(&k_wheel_peer<D, 4>)};
   const char* co = getenv("WCSP_CARVEOUT");       // A/B runs: shared-memory carveout in percent of L1
   for (void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -578,6 +578,7 @@ struct SlabSpec {
   const uint8_t* ghost;            // host [N_local]
   unsigned long long nB;
   int f1max;
+  int per_sm;                      // > 0: blocks per SM of the slab's grid (peer halo, 4-block build)
 };
 
 wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const SlabSpec* spec, wcsp_handle** out) {
@@ -625,6 +626,7 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
                                                     sizeof(Smem)));
   if (per_sm < 1) CKH(fail(WCSP_ECUDA, "cycle kernel cannot be resident"));
   if (bps) per_sm = std::max(1, std::min(per_sm, atoi(bps)));
+  if (spec && spec->per_sm > 0) per_sm = spec->per_sm;     // peer-halo slab: sized for the peer kernel
   h->grid = per_sm * h->nsm;
   const size_t fb = (size_t)h->d * N;
   CKC(cudaMalloc(&h->d_f1, fb));
@@ -762,7 +764,7 @@ wcsp_status host_validate(const wcsp_problem* p, unsigned long long* nB, int* f1
   return WCSP_REACHED;
 }
 
-void* peer_fn_d(int d);
+void* peer_fn_d(int d, bool big);
 wcsp_status peer_connect(wcsp_handle* g);
 
 wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_handle** out) {
@@ -778,6 +780,10 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
   long long N = 1;
   for (int k = 0; k < d; ++k) N *= p->shape[k];
   const long long plane = N / nL;
+  // peer halo on 3-D grids >= 2^21 vertices: the 4-blocks-per-SM build of the fused kernel (as
+  // k_wheel_persistent); every slab handle is then sized for it
+  const char* bps = getenv("WCSP_BLOCKS_PER_SM");
+  const bool peer_big = opt.halo == WCSP_HALO_PEER && (bps ? atoi(bps) >= 4 : d >= 3 && N >= (1ll << 21));
   unsigned long long nB = 0;
   int f1max = 1;
   wcsp_status st = host_validate(p, &nB, &f1max);
@@ -817,6 +823,7 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
     sp.plane = (unsigned)plane;
     sp.nB = nB;
     sp.f1max = f1max;
+    sp.per_sm = peer_big ? 4 : 0;
     std::vector<uint8_t> f1((size_t)d * Nl), f2((size_t)d * Nl), A(Nl), B(Nl), ghost(Nl, 0), pres;
     for (int k = 0; k < d; ++k) {
       memcpy(&f1[(size_t)k * Nl], p->f1 + (size_t)k * N + lo, Nl);
@@ -867,12 +874,13 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
     if (!dist && R > MAX_VSLABS) return bail(fail(WCSP_EINVAL, "at most %d virtual slabs with the peer halo", MAX_VSLABS));
     int per_sm = 0, nsm = 0;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->dev) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peer_fn_d(d), THREADS, sizeof(Smem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, peer_fn_d(d, peer_big), THREADS, sizeof(Smem)) != cudaSuccess ||
         per_sm < 1)
       return bail(fail(WCSP_ECUDA, "peer-halo kernel cannot be resident"));
     const int per = std::min(g->grid, per_sm * nsm / (dist ? 1 : R));
     if (per < 1) return bail(fail(WCSP_EINVAL, "too many slabs for one device"));
     g->halo = WCSP_HALO_PEER;
+    g->big = peer_big;
     g->peer_per = (unsigned)per;
     if (cudaMalloc(&g->xbar, 4 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMemset(g->xbar, 0, 4 * sizeof(unsigned long long)) != cudaSuccess)
@@ -1209,9 +1217,12 @@ Dev make_peer_dev(wcsp_handle* g, int i) {
   return s;
 }
 
-void* peer_fn_d(int d) {
-  return d == 1 ? reinterpret_cast<void*>(&k_wheel_peer<1>) : d == 2 ? reinterpret_cast<void*>(&k_wheel_peer<2>)
-       : d == 3 ? reinterpret_cast<void*>(&k_wheel_peer<3>) : reinterpret_cast<void*>(&k_wheel_peer<4>);
+template <int D>
+void* peer_fn(bool big) {
+  return big ? reinterpret_cast<void*>(&k_wheel_peer<D, 4>) : reinterpret_cast<void*>(&k_wheel_peer<D, 3>);
+}
+void* peer_fn_d(int d, bool big) {
+  return d == 1 ? peer_fn<1>(big) : d == 2 ? peer_fn<2>(big) : d == 3 ? peer_fn<3>(big) : peer_fn<4>(big);
 }
 
 wcsp_status peer_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
@@ -1238,7 +1249,7 @@ wcsp_status peer_solve_once(wcsp_handle* g, wcsp_result* r, int* status) {
   set.n = n;
   for (int i = 0; i < n; ++i) set.d[i] = make_peer_dev(g, i);
   void* args[] = {&set};
-  CK(cudaLaunchCooperativeKernel(peer_fn_d(g->d), dim3(n * g->peer_per), dim3(THREADS), args, sizeof(Smem),
+  CK(cudaLaunchCooperativeKernel(peer_fn_d(g->d, g->big), dim3(n * g->peer_per), dim3(THREADS), args, sizeof(Smem),
                                  g->stream));
   g->launches += 1;
   return dist ? dist_collect(g, r, status) : group_collect(g, r, status);

@@ -738,9 +738,9 @@ __device__ __forceinline__ void window_emit(const Dev& s, unsigned bits, unsigne
 // ---------------------------------------------------------------------------
 template <int D, bool WHEEL_ENGINE, bool PEER = false>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
-                                          unsigned& dmin, unsigned long long& created,
-                                          unsigned long long& relabels, unsigned long long& triggered,
-                                          unsigned long long& lanes_started, unsigned long long& tested);
+                                          unsigned& dmin, unsigned& created,
+                                          unsigned& relabels, unsigned& triggered,
+                                          unsigned& lanes_started, unsigned& tested);
 
 __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
   return ((texp16 - (unsigned)t) & 0xFFFFu) - 1u < 255u;   // texp in (t, t + 255]
@@ -761,9 +761,6 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #ifndef WCSP_WIN_PREFETCH
 #define WCSP_WIN_PREFETCH 0        // 1: the next round's bitmap words load while this round is treated (no gain; off)
 #endif
-#ifndef WCSP_STAGE_BITLOOP
-#define WCSP_STAGE_BITLOOP 0       // 1: stage a vertex's events in a loop over its passed directions
-#endif
 #ifndef WCSP_TREAT_AGG
 #define WCSP_TREAT_AGG 1           // one warp-scan staging reservation per treat batch (not one per lane direction)
 #endif
@@ -779,9 +776,9 @@ __device__ void regions_close(const Dev& s, Smem& sm, long long t);
 
 template <int D, bool WHEEL_ENGINE, bool PEER>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
-                                          unsigned& dmin, unsigned long long& created,
-                                          unsigned long long& relabels, unsigned long long& triggered,
-                                          unsigned long long& lanes_started, unsigned long long& tested) {
+                                          unsigned& dmin, unsigned& created,
+                                          unsigned& relabels, unsigned& triggered,
+                                          unsigned& lanes_started, unsigned& tested) {
   using LW = typename Tr<D>::LW;
   const bool valid = q != 0xFFFFFFFFu;
   tested += valid;
@@ -885,19 +882,6 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       if (lane == 31) base = atomicAdd(&sm.np, tot);
       base = __shfl_sync(0xFFFFFFFFu, base, 31);
       unsigned idx = base + x - cnt;
-#if WCSP_STAGE_BITLOOP
-      // only the passed directions (popc(pm) iterations, not 2d predicated ones)
-      const unsigned long long rc = (unsigned long long)q | ((unsigned long long)(inactive ? 1u : 0u) << 49);
-      for (unsigned m = pm; m; m &= m - 1u) {
-        const unsigned j = (unsigned)__ffs(m) - 1u;
-        const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
-        const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
-        ev_stage(s, sm, idx++,
-                 rc | ((unsigned long long)j << PH_LANE) | ((unsigned long long)(unsigned)(lstar - (int)f2j) << PH_CAND) |
-                     ((unsigned long long)((spm >> j) & 1u) << 50),
-                 f1j, v.t);
-      }
-#else
 #pragma unroll
       for (int j = 0; j < 2 * D; ++j) {
         if ((pm >> j) & 1u) {
@@ -910,7 +894,6 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
           ev_stage(s, sm, idx++, rec, f1j, v.t);
         }
       }
-#endif
     }
   }
 #endif
@@ -941,7 +924,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   const unsigned rounds = (nwin + s.nblocks * WARPS - 1) / (s.nblocks * WARPS);
   const unsigned win0 = (blockIdx.x - s.blk0) * rounds * WARPS;
   unsigned dmin = 0xFFFFFFFFu;
-  unsigned long long created = 0, relabels = 0, triggered = 0, lanes_started = 0, tested = 0;
+  unsigned created = 0, relabels = 0, triggered = 0, lanes_started = 0, tested = 0;   // per thread, this cycle
   if constexpr (WHEEL_ENGINE) {
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
       sm.rcap[d] = 0; sm.rfill[d] = 0; sm.ofill[d] = 0;

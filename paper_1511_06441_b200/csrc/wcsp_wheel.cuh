@@ -285,7 +285,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   unsigned long long* dpos = reinterpret_cast<unsigned long long*>(&sm.wl[0][0]);   // [MAXD]
   unsigned* dchunk = reinterpret_cast<unsigned*>(dpos + MAXD);                        // [MAXD + 1] prefix
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  unsigned long long arr = 0;
+  unsigned arr = 0;
   // Dense cycles: first arrivals near the block's own slab of the grid (its treat windows and one
   // plane of the last axis on either side: where the events it fires lead) set bits of a
   // shared-memory bitmap (the treat staging is free during the fire), merged into the global
@@ -898,8 +898,8 @@ __device__ __forceinline__ bool peer_sync(const Dev& s, Smem& sm, unsigned long 
   return ok;
 }
 
-template <int D>
-__global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_peer(const __grid_constant__ DevSet set) {
+template <int D, int MINB = WCSP_MINB>   // MINB: as k_wheel_persistent
+__global__ void __launch_bounds__(THREADS, MINB) k_wheel_peer(const __grid_constant__ DevSet set) {
   const Dev& s = set.d[blockIdx.x / set.per];
   Smem& sm = smem();
   init_smem(sm);

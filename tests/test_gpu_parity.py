@@ -528,3 +528,22 @@ def test_C5_full_size_one_gpu():
         assert (r_lo.F1, r_lo.F2) == (g["F1_at_F2min"], g["F2_min"])
         s.set_targets(M=g["F2_min"])
         assert s.solve().status == wcsp.INFEASIBLE
+
+
+@pytest.mark.parametrize("bps", ["3", "4"])
+def test_both_cycle_kernel_builds(bps, monkeypatch):
+    """The persistent wheel kernel exists in two builds (4 resident blocks per SM,
+    64 registers, taken for 3-D grids >= 2^21 vertices; 3 blocks, 80 registers, otherwise).
+    WCSP_BLOCKS_PER_SM forces either; both must give the oracle's outputs and tier 5's counters,
+    on random small cases and on face-to-face cubes that span several treat rounds per block."""
+    monkeypatch.setenv("WCSP_BLOCKS_PER_SM", bps)
+    rng = np.random.default_rng(909)
+    for _ in range(40):
+        inst = I.random_small(rng, shapes=[(6, 5, 4), (10, 10, 10), (16, 16), (3, 3, 3, 3)], M_range=(5, 120),
+                              max_sources=4, max_targets=4, hole_prob=0.1)
+        check(inst, "wheel")
+    for shape, seed, M in [((40, 40, 40), 1, 200), ((64, 48, 32), 2, 260), ((128, 96), 3, 500)]:
+        r, _ = check(I.config_face(shape, seed, M), "wheel")
+        for slabs in (2, 4):         # the fused peer-halo kernel comes in the same two builds
+            rp = wcsp.solve(I.config_face(shape, seed, M), engine="wheel", slabs=slabs, halo="peer")
+            assert rp.key() == r.key() and model_counters(rp) == model_counters(r), (shape, slabs, rp, r)

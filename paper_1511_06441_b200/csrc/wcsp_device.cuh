@@ -41,6 +41,9 @@ constexpr int CHUNK_MAX = THREADS * SWEEP_ITEMS;
 #ifndef WCSP_MINB_SWEEP
 #define WCSP_MINB_SWEEP 4          // resident blocks per SM the sweep engine's kernels are compiled for
 #endif
+#ifndef WCSP_BAR_GROUPS
+#define WCSP_BAR_GROUPS 1          // > 1: two-level grid-barrier arrivals (per-group counters)
+#endif
 #ifndef WCSP_QP_CAP
 #define WCSP_QP_CAP 3072
 #endif
@@ -115,6 +118,7 @@ struct Ctl {
   long long stair_q;               // best target quality so far
   alignas(128) unsigned long long grel;   // grid barrier: the last block to arrive releases this target
   unsigned long long pad4_[15];           // (its own 128-byte line: pollers do not slow the arrivals)
+  alignas(128) unsigned long long bsub[WCSP_BAR_GROUPS][16];   // WCSP_BAR_GROUPS > 1: per-group arrivals
 };
 
 struct TraceRec {
@@ -1115,6 +1119,9 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // BARRIER_TIMEOUT_NS sets ctl->abort; every waiting block then gives up).
 constexpr unsigned long long BARRIER_TIMEOUT_NS = 20ull * 1000000000ull;
 
+#ifndef WCSP_BAR_SLEEP
+#define WCSP_BAR_SLEEP 32          // ns between polls of the grid barrier
+#endif
 #ifndef WCSP_BAR_RELEASE
 #define WCSP_BAR_RELEASE 0         // 1: the last arriver releases a flag on its own line (measured: C2 +8 %; off)
 #endif
@@ -1138,6 +1145,19 @@ __device__ __forceinline__ bool grid_sync(Ctl* ctl, unsigned long long target, S
       st_release_gpu(&ctl->grel, target);
     }
     unsigned long long* const poll = &ctl->grel;
+#elif WCSP_BAR_GROUPS > 1
+    // two-level arrival: blocks count on one of WCSP_BAR_GROUPS lines; the last of each group adds
+    // the group's size to ctl->bar (fewer same-address atomics serialised at one L2 slice)
+    {
+      const unsigned NGp = WCSP_BAR_GROUPS, G = gridDim.x, g = blockIdx.x % NGp;
+      const unsigned long long gk = (G - g + NGp - 1) / NGp;          // blocks in group g
+      const unsigned long long epoch = target / G;
+      if (atomicAdd(&ctl->bsub[g][0], 1ull) == epoch * gk - 1) {
+        __threadfence();
+        atomicAdd(&ctl->bar, gk);
+      }
+    }
+    unsigned long long* const poll = &ctl->bar;
 #else
     atomicAdd(&ctl->bar, 1ull);
     unsigned long long* const poll = &ctl->bar;
@@ -1145,7 +1165,7 @@ __device__ __forceinline__ bool grid_sync(Ctl* ctl, unsigned long long target, S
     const unsigned long long t0 = globaltimer_ns();
     unsigned ok = 1;
     while (ld_acquire(poll) < target) {
-      __nanosleep(32);
+      if (WCSP_BAR_SLEEP > 0) __nanosleep(WCSP_BAR_SLEEP);
       if (*(volatile unsigned*)&ctl->abort) { ok = 0; break; }
       if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&ctl->abort, 1u); ok = 0; break; }
     }

@@ -48,6 +48,16 @@ constexpr unsigned MAINT_PERIOD_T = 1u << 15;
 #define WCSP_MINB 3                       // resident blocks per SM the cycle kernels are compiled for
 #endif
 constexpr int FIRE_ITEMS = WCSP_FIRE_ITEMS;   // events per lane per fire chunk (atomics in flight)
+// dense cycles, per build of the persistent kernel: the 4-blocks-per-SM build (3-D grids >= 2^21
+// vertices) fires 12 events per lane (C3 135.1 -> 133.8 ms), the 3-block build 6 (C2 97.0 -> 95.1
+// ms; profiles/r01/ab_v14_fire_hints.txt); sparse cycles of the 3-block build keep FIRE_ITEMS (C4 23.3 vs 26.3 ms at 6)
+#ifndef WCSP_FIRE_ITEMS_4B
+#define WCSP_FIRE_ITEMS_4B 12
+#endif
+#ifndef WCSP_FIRE_ITEMS_3B
+#define WCSP_FIRE_ITEMS_3B 6
+#endif
+template <int MINB> __host__ __device__ constexpr int fire_items() { return MINB >= 4 ? WCSP_FIRE_ITEMS_4B : WCSP_FIRE_ITEMS_3B; }
 
 // Runs are filed per (bucket, block): the block that treats a slab of the grid
 // also fires the events its slab created, so the atomics of a fire phase
@@ -271,7 +281,7 @@ __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
 // fires the runs its own slab filed; the runs are cut into chunks of
 // FIRE_ITEMS * 32 events that the block's warps take in turn (a prefix sum of
 // chunk counts over the block's runs lives in shared memory).
-template <int D, bool PEER = false>
+template <int D, bool PEER = false, int FI = FIRE_ITEMS>   // FI: events per lane per chunk
 __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   Acc* acc = &s.ctl->acc[v.c % 3];
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
@@ -280,7 +290,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   const size_t slot = (size_t)b * s.nblocks + vb;
   const unsigned nd = min(__ldcg(s.bndesc + slot), s.dcap);
   const unsigned long long* dl = s.bdesc + slot * s.dcap;
-  constexpr unsigned CH = FIRE_ITEMS * 32;
+  constexpr unsigned CH = FI * 32;
   constexpr unsigned MAXD = 512;
   unsigned long long* dpos = reinterpret_cast<unsigned long long*>(&sm.wl[0][0]);   // [MAXD]
   unsigned* dchunk = reinterpret_cast<unsigned*>(dpos + MAXD);                        // [MAXD + 1] prefix
@@ -356,28 +366,28 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
       di = lo;
     }
     // chunk c's events: descriptor di (advanced monotonically), FIRE_ITEMS per lane
-    auto load_chunk = [&](unsigned c, unsigned long long (&ev)[FIRE_ITEMS]) {
+    auto load_chunk = [&](unsigned c, unsigned long long (&ev)[FI]) {
       while (dchunk[di + 1] <= c) ++di;
       const unsigned long long dsc = dpos[di];
       const unsigned long long pos = dsc >> 24;
       const unsigned cnt = (unsigned)(dsc & 0xFFFFFFu);
       const unsigned base = (c - dchunk[di]) * CH;
 #pragma unroll
-      for (int it = 0; it < FIRE_ITEMS; ++it) {
+      for (int it = 0; it < FI; ++it) {
         const unsigned i = base + it * 32 + lane;
         ev[it] = i < cnt ? ld_hint(s.ev + ((pos + i) & s.ev_mask), pol_first()) : ~0ull;
       }
     };
-    unsigned long long e[FIRE_ITEMS];
+    unsigned long long e[FI];
     if (c_lo < c_hi) load_chunk(c_lo, e);
     for (unsigned c = c_lo; c < c_hi; ++c) {
 #if WCSP_FIRE_PF
-      unsigned long long en[FIRE_ITEMS];   // the next chunk's events load while this one fires
+      unsigned long long en[FI];   // the next chunk's events load while this one fires
       if (c + 1 < c_hi) load_chunk(c + 1, en);
 #endif
-      unsigned old[FIRE_ITEMS];
+      unsigned old[FI];
 #pragma unroll
-      for (int it = 0; it < FIRE_ITEMS; ++it) {   // put every atomic in flight before using a result
+      for (int it = 0; it < FI; ++it) {   // put every atomic in flight before using a result
         const bool valid = e[it] != ~0ull;
         arr += valid;
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
@@ -416,7 +426,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         old[it] = arrive_atomic<PEER>(s, v, valid, src + s.off[ln], (int)((e[it] >> PH_CAND) & 0xFFFFu));
       }
 #pragma unroll
-      for (int it = 0; it < FIRE_ITEMS; ++it) {
+      for (int it = 0; it < FI; ++it) {
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
         const unsigned via = ((e[it] >> EV_LANE_BIT) & 1) ? 0u : 1u;
@@ -425,7 +435,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
       }
 #if WCSP_FIRE_PF
 #pragma unroll
-      for (int it = 0; it < FIRE_ITEMS; ++it) e[it] = en[it];
+      for (int it = 0; it < FI; ++it) e[it] = en[it];
 #else
       if (c + 1 < c_hi) load_chunk(c + 1, e);
 #endif
@@ -740,7 +750,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_persistent(Dev s) {
     if (v.c > 0) {
       if (blockIdx.x == 0 && threadIdx.x == 0) wheel_cycle_start(s, v);
       if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
-      wheel_fire<D>(s, v, sm);
+      // 3-block build: sparse cycles (thin fronts) keep FIRE_ITEMS; the 4-block build has no
+      // registers for a second copy of the fire (spills) and fires 12 per lane throughout
+      if (MINB < 4 && v.lmode) wheel_fire<D, false, FIRE_ITEMS>(s, v, sm);
+      else wheel_fire<D, false, fire_items<MINB>()>(s, v, sm);
       target += G;
       if (!grid_sync(s.ctl, target, sm, s.trace_cap > 0 ? &s.ctl->fin[v.c & 1][0][0] : nullptr)) return;
     }

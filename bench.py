@@ -9,9 +9,13 @@ in HBM.  Prints ONE JSON line (rank 0).
 Metric (BASELINE.json): active edge-updates/s = sum over cycles of (live active
 edges + live phantom edges) / solve time; also reported: solve
 time, and achieved HBM GB/s of the cycle kernel against MEASURED_PEAKS.json.
-Multi-GPU (N > 1, torchrun): every rank solves its own seed of the workload
-(independent instances, no data-path collective; weak scaling); the time is
-the max over ranks.
+Multi-GPU (N > 1): `--gpus N` without torchrun re-launches this script under
+torch.distributed.run with N ranks (one per GPU); under torchrun WORLD_SIZE
+must equal N.  Default partition: the ONE instance cut into N z-slabs (SURVEY
+§8(e); boundary fused over NVLink peer memory in one persistent kernel per GPU,
+`--halo copy` for NCCL send/recv per cycle) — strong scaling; `--partition
+replicas` solves an independent seed per rank instead (weak scaling).  The time
+is the max over ranks of the device time.
 """
 from __future__ import annotations
 
@@ -48,7 +52,7 @@ for _side in (50, 75, 100, 125):   # the §6 protocol: water on t
                                                              f"f1,f2 ~ U{{1..10}}, M = M_bind"}
     WORKLOADS[f"P6-{_side}-inf"] = {"shape": (_side,) * 3, "desc": f"§6 cube {_side}^3, boundary -> centre, "
                                                                  f"f1 ~ U{{1..10}}, M = infinity"}
-MBIND = os.path.join(ROOT, "paper_1511_06441_b200", "data", "mbind.json")
+MBIND = os.path.join(ROOT, "tests", "golden", "mbind.json")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "roofline_traffic.json")
 
 
@@ -96,21 +100,26 @@ def reduce_timing(total_ms: float, units: float, device: str):
     return float(t.item()), float(u.item())
 
 
-def alg_bytes(r, d: int, engine: str) -> int:
-    """Algorithmic bytes per solve.
-    sweep engines (SURVEY §8(d) 'alg'): 2 B per live lane/phantom per cycle
-      (u8 residual read + write), 13 B per arrival, (2d*8 + 22) B per triggered
-      vertex, 8 B per phantom created, 2 B per relabel.
-    wheel engines (events are not touched between creation and arrival):
-      8 B written per event created (lanes started + phantoms), 8 B read +
-      8 B temp read-modify-write per arrival, (8 + 16 + 2d*8) B per triggered
-      vertex (its state word, weight record, neighbours' state words), 4 B per
-      relabel."""
-    if engine.startswith("wheel"):
-        return (8 * (r.lanes_started + r.phantoms_created) + 16 * r.arrivals + (24 + 2 * d * 8) * r.triggered
-                + 4 * r.relabels)
+def alg_bytes(r, d: int) -> int:
+    """Algorithmic bytes per solve: SURVEY §8(d) 'alg', per cycle
+        2 (E + P) + 13 R + (2d*8 + 22) T + 8 C + 2 RL
+    summed over the solve's cycles = the same formula on the solve's totals:
+    2 B per live lane/phantom per cycle (u8 residual read + write), 13 B per
+    arrival (L(src) 2, f2 1, L(D) 2, temp atomic 8), 2d*8 + 22 B per triggered
+    vertex (neighbour label + temp, f1/f2, own lane word r/w, label write, list
+    read), 8 B per phantom created, 2 B per relabel.  E + P = edge_updates,
+    R = arrivals, T = triggered, C = phantoms_created, RL = relabels."""
     return (2 * r.edge_updates + 13 * r.arrivals + (2 * d * 8 + 22) * r.triggered + 8 * r.phantoms_created
             + 2 * r.relabels)
+
+
+def wheel_bytes(r, d: int) -> int:
+    """The timing-wheel engine's own byte model (events are not
+    touched between creation and arrival): 8 B written per event created, 8 B
+    read + 8 B temp read-modify-write per arrival, (24 + 2d*8) B per triggered
+    vertex, 4 B per relabel.  Reported beside the §8(d) numerator."""
+    return (8 * (r.lanes_started + r.phantoms_created) + 16 * r.arrivals + (24 + 2 * d * 8) * r.triggered
+            + 4 * r.relabels)
 
 
 class ClockSampler:
@@ -161,51 +170,132 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def cpu_sample(inst, target_s: float = 15.0):
-    """The oracle (tier 2, as it stands) on a bounded sample of the same workload:
-    the first t_limit time units of the same instance, t_limit grown until the
-    run takes about target_s seconds on one host core.  Value = the oracle's own
-    count of flows in flight summed over event times (the same quantity as the
-    metric's numerator, on the oracle's pruned flow set) / CPU seconds."""
+def host_cpu():
+    """(nproc, CPU model) of this host."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count(), model
+
+
+def sample_instance(workload: str, side: int):
+    """A bounded sample of the workload: the same recipe (value distribution, A/B
+    rule, dimension, budget rule) on a cube of `side`; M_bind by the oracle's
+    tier 3 (two lexicographic Dijkstras, SURVEY §8 notation)."""
+    from paper_1511_06441_b200 import instances as I
     import oracle
-    t_limit, r, dt = 4, None, 0.0
-    while True:
-        t0 = time.perf_counter()
-        r = oracle.solve_pruned(inst, t_limit=t_limit)
-        dt = time.perf_counter() - t0
-        if dt >= target_s / 3 or r.status != oracle.ELIMIT:
-            break
-        t_limit = int(t_limit * max(1.5, min(8.0, target_s / max(dt, 1e-3))))
-    return r, dt, t_limit
+    if workload == "C4":
+        k = max(3, min(10, side.bit_length() - 1))
+        return I.fractal_instance(k), f"Theorem-2 fractal k = {k} (t = {1 << k}), M = infinity"
+    d = len(WORKLOADS[workload]["shape"])
+    shape = (side,) * d
+    if workload.startswith("P6-"):
+        inst = I.grid_instance(shape, 0, 1, 10, "boundary", "centre", I.M_INF, workload)
+        if workload.endswith("-inf"):
+            return inst, f"{'x'.join(map(str, shape))} cube of the §6 recipe, M = infinity"
+    else:
+        inst = I.config_face(shape, 0, I.M_INF, name=workload)
+    Mb = oracle.m_bind(inst)
+    return inst.with_M(Mb), f"{'x'.join(map(str, shape))} grid of the {workload} recipe (seed 0, M_bind = {Mb})"
+
+
+SIDES = {2: [64, 96, 128, 192, 256, 384, 512], 3: [24, 32, 40, 48, 56, 64, 72, 80, 96]}
+
+
+def pick_side(workload: str, target_s: float) -> int:
+    """The largest sample side whose tier-5 solve is predicted to take at most
+    target_s (calibrated on the smallest; cost ~ N * cycles ~ side^(d+1))."""
+    import oracle
+    d = 2 if workload in ("C2", "C4") else 3
+    sides = SIDES[d]
+    inst, _ = sample_instance(workload, sides[0])
+    t0 = time.perf_counter()
+    oracle.solve_model(inst)
+    dt0 = max(time.perf_counter() - t0, 1e-3)
+    side = sides[0]
+    for s_ in sides[1:]:
+        if dt0 * (s_ / sides[0]) ** (d + 1) <= target_s:
+            side = s_
+    return side
+
+
+def cpu_sample(workload: str, target_s: float):
+    """The CPU baseline: oracle tier 5 — the paper's nine-step cycle run
+    sequentially on one host core (oracle/wcsp_oracle.c orc_model, as it stands)
+    — solving a bounded sample of the workload in full: the same recipe on the
+    largest cube predicted to take at most target_s.  Its work counter is the
+    metric's numerator by the same definition (sum over cycles of live edges +
+    live phantoms; equal to the GPU's counters bit for bit where both run), so
+    value = work / CPU seconds is directly comparable with `value`."""
+    import oracle
+    inst, what = sample_instance(workload, pick_side(workload, target_s))
+    t0 = time.perf_counter()
+    r, c = oracle.solve_model(inst)
+    dt = time.perf_counter() - t0
+    nproc, model = host_cpu()
+    return {"value": c.work / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle tier 5 (the paper's cycle run sequentially, oracle/wcsp_oracle.c orc_model) solving "
+                      f"the {what} in full: {c.work} edge-updates over {c.cycles} cycles in {dt:.2f} s",
+            "seconds": round(dt, 3), "host_nproc": nproc, "host_cpu": model}
+
+
+def cpu_full(inst):
+    """The oracle's time to solution on the bench instance itself (tier 2, one
+    core, in full); run in a child process concurrently with the GPU steps
+    (--cpu-full; about 6-10 minutes on C3)."""
+    import oracle
+    t0 = time.perf_counter()
+    o = oracle.solve_pruned(inst)
+    return {"tier": 2, "seconds": round(time.perf_counter() - t0, 2), "key": list(o.key()), "cores": 1}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle on the host cores, bounded samples."""
+    """--impl reference: the CPU oracle (tier 5, as it stands) on the host cores,
+    each step one bounded sample of the workload (see cpu_sample), sized so the
+    whole W + K run stays within about three minutes."""
     if rank != 0:
         return
-    inst, meta = workload_instance(args.workload, 0)
     import oracle
     oracle.build()
-    # each step a bounded sample sized so the whole W + K run stays within ~2.5 minutes
-    r, dt, t_limit = cpu_sample(inst, target_s=min(args.ref_seconds, 150.0 / max(1, args.warmup + args.steps)))
+    per_step = min(args.ref_seconds, 150.0 / max(1, args.warmup + args.steps))
+    inst, what = sample_instance(args.workload, pick_side(args.workload, per_step))
     times, work = [], []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        rr = oracle.solve_pruned(inst, t_limit=t_limit)
-        d = time.perf_counter() - t0
+        _, c = oracle.solve_model(inst)
+        dt = time.perf_counter() - t0
         if i >= args.warmup:
-            times.append(d)
-            work.append(rr.work)
+            times.append(dt)
+            work.append(c.work)
     value = sum(work) / sum(times)
-    sample = f"first {t_limit} time units of {args.workload} seed {meta['seed']} (t_final of the full solve ~{meta['F1_lex']}+)"
+    nproc, model = host_cpu()
+    sample = (f"oracle tier 5 (the paper's cycle run sequentially, one core) solving the {what} in full per step "
+              f"({work[0]} edge-updates); host {nproc} cores, {model}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic", "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
-                                            "seed": meta["seed"], "M": inst.M, "sample": sample},
+                                            "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run
+    with N ranks (rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -217,31 +307,47 @@ def main():
     ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--engine", default="wheel", choices=["persistent", "stepped", "wheel", "wheel_stepped"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="also time the oracle (tier 2) solving the bench instance in full, concurrently")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--partition", default="replicas", choices=["replicas", "slabs"],
-                    help="N > 1: independent seeds per rank (weak) or one instance cut into z-slabs (strong)")
+    ap.add_argument("--partition", default="slabs", choices=["replicas", "slabs"],
+                    help="N > 1: one instance cut into N z-slabs (strong scaling, default) or an independent "
+                         "seed per rank (weak scaling)")
     ap.add_argument("--halo", default="peer", choices=["copy", "peer"],
                     help="slab boundary: fused over peer memory in one kernel (peer) or ghost-plane copies")
     ap.add_argument("--vslabs", type=int, default=0,
                     help="N = 1: cut the instance into this many virtual slabs on the one GPU")
     args = ap.parse_args()
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
+    if world != args.gpus and not (args.impl == "reference" and "WORLD_SIZE" not in os.environ):
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE = {world} (launch one rank per GPU)\n")
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
 
+
+def run_ours(args, rank, world, local):
     import torch
+    slabs = world > 1 and args.partition == "slabs"
+    if world > 1:
+        # NCCL's communicator lines (rank, nranks, transport) for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1511_06441_b200 import wcsp
 
-    slabs = world > 1 and args.partition == "slabs"
     inst, meta = workload_instance(args.workload, 0 if slabs else rank)
     d = len(inst.shape)
     stream = torch.cuda.current_stream()
-    if slabs:   # one instance, slab `rank` of `world` on this GPU, NCCL exchange every cycle
+    if slabs:   # one instance, slab `rank` of `world` on this GPU
         solver = wcsp.Solver(inst, engine="wheel", stream=stream, nranks=world, rank=rank,
                              nccl_id=share_nccl_id(rank), halo=args.halo)
     elif args.vslabs > 1:
@@ -249,6 +355,12 @@ def main():
     else:
         solver = wcsp.Solver(inst, engine=args.engine, stream=stream)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > L2 (126 MB)
+
+    full = None
+    if args.cpu_full and rank == 0:          # the oracle's full solve runs beside the GPU steps
+        import multiprocessing as mpc
+        full = mpc.get_context("fork").Pool(1)
+        full_res = full.apply_async(cpu_full, (inst,))
 
     for _ in range(args.warmup):
         solver.solve()
@@ -259,7 +371,7 @@ def main():
         torch.cuda.synchronize()
 
     # timed region: K solves, L2 flushed between steps (outside the events)
-    results, step_ms = [], []
+    results = []
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     with ClockSampler(local) as clocks:
@@ -279,25 +391,32 @@ def main():
         updates_all = updates
     value = updates_all / (total_ms / 1000.0)
 
-    # roofline of the dominant kernel (the cycle kernel; one launch per solve)
+    # roofline of the dominant kernel (the persistent cycle kernel; one launch per solve)
     r0 = results[0]
     cyc_ms = statistics.mean(r.cycle_ms for r in results)
-    ab = alg_bytes(r0, d, args.engine)
+    ab = alg_bytes(r0, d)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = ab / (cyc_ms / 1000.0) / 1e9
-    traffic = None
+    traffic, dram_src = None, None
     if os.path.exists(PROFILE_SUMMARY):
         try:
             ps = json.load(open(PROFILE_SUMMARY)).get(f"{args.workload}/{args.engine}")
-            traffic = ps["dram_bytes_per_launch"] if ps else None
+            if ps:
+                traffic, dram_src = ps["dram_bytes_per_launch"], ps.get("source")
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": {"persistent": "k_persistent<D>", "wheel": "k_wheel_persistent<D>"}.get(args.engine, "k_*<D> (stepped: 3 launches per cycle)") + " (cycle kernel)",
+                "kernel": {"persistent": "k_persistent<D>", "wheel": "k_wheel_persistent<D>"}.get(
+                    args.engine, "k_*<D> (stepped: 3 launches per cycle)") + " (cycle kernel)",
                 "alg_bytes_per_launch": ab,
+                "alg_formula": "SURVEY §8(d): 2(E+P) + 13R + (2d*8+22)T + 8C + 2RL over the solve's counters",
+                "wheel_model_bytes_per_launch": wheel_bytes(r0, d),
+                "wheel_model_gbs": round(wheel_bytes(r0, d) / (cyc_ms / 1000.0) / 1e9, 2),
+                "dram_gbs": round(traffic / (cyc_ms / 1000.0) / 1e9, 2) if traffic else None,
+                "dram_source": dram_src,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback B200_PROFILING.md 6.65 TB/s"}
 
     # e2e through the C-ABI with host buffers (pinned): H2D of the step's inputs + solve + result read
@@ -323,18 +442,19 @@ def main():
         if world > 1:
             et, e_upd = reduce_timing(et, e_upd / world if slabs else e_upd, "cuda")
         e2e = {"value": e_upd / (et / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": 312, "ms_per_step": et / args.e2e_steps,
-               "path": "wcsp_load (pinned host f1,f2,A,B -> HBM, validate, weight build) + wcsp_solve + result D2H"}
+               "d2h_bytes_per_step": 5120, "ms_per_step": et / args.e2e_steps,
+               "path": "wcsp_load (pinned host f1,f2,A,B -> HBM, validate, weight build) + wcsp_solve + result "
+                       "D2H (the 5120-byte control block, sizeof(Ctl))"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r, dt, t_limit = cpu_sample(inst)
-        import oracle
-        what = (f"the first {t_limit} time units of the same instance" if r.status == oracle.ELIMIT
-                else "the whole instance")
-        cpu = {"value": r.work / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"oracle tier 2 (oracle/wcsp_oracle.c orc_pruned) on {what} "
-                         f"({dt:.2f} s, {r.work} flow-updates, {r.cycles} event times)"}
+        cpu = cpu_sample(args.workload, args.cpu_seconds)
+    cpu_full_rec = None
+    if full is not None:
+        cpu_full_rec = full_res.get()
+        cpu_full_rec["matches_gpu"] = cpu_full_rec["key"] == list(r0.key())
+        cpu_full_rec["gpu_speedup_time_to_solution"] = round(cpu_full_rec["seconds"] * 1000.0 / (total_ms / args.steps), 1)
+        full.close()
 
     if rank == 0:
         line = {
@@ -343,7 +463,7 @@ def main():
             "scaling": "strong" if slabs else "weak", "vs_baseline": None, "dtype": "u16", "data": "synthetic",
             "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
                        "shape": list(inst.shape), "seed": meta["seed"], "M": inst.M,
-                       "M_bind_from": "paper_1511_06441_b200/data/mbind.json (oracle, scripts/make_mbind.py)",
+                       "M_bind_from": "tests/golden/mbind.json (oracle, scripts/make_mbind.py)",
                        "engine": args.engine, "l2": "flushed between steps (256 MiB write outside the events)",
                        "parallelism": (f"{world} z-slabs of one instance ("
                                        + ("boundary fused over NVLink peer memory, one kernel per GPU"
@@ -355,11 +475,12 @@ def main():
             "solve": {"F1": r0.F1, "F2": r0.F2, "X": r0.X, "Y": r0.Y, "cycles": r0.cycles,
                       "edge_updates": r0.edge_updates, "arrivals": r0.arrivals, "triggered": r0.triggered,
                       "phantoms_created": r0.phantoms_created, "relabels": r0.relabels,
-                      "peak_active": r0.peak_active, "peak_phantoms": r0.peak_phantoms,
-                      "cycle_ms": r0.cycle_ms, "device_ms": r0.device_ms},
+                      "lanes_started": r0.lanes_started, "peak_phantoms": r0.peak_phantoms,
+                      "cycle_ms": r0.cycle_ms, "device_ms": r0.device_ms, "retries": r0.retries},
             "hbm_gbs_alg": round(achieved, 2),
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "cpu_full": cpu_full_rec,
             "e2e": e2e,
             "gpu_launches": int(sum(r.kernel_launches for r in results)),
             "clocks": clocks.summary(),
@@ -371,4 +492,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

@@ -57,7 +57,13 @@ typedef enum {
 } wcsp_status;
 
 #define WCSP_M_INF (-1)           /* M = +infinity: first passage */
-#define WCSP_M_MAX 65533          /* largest finite M (16-bit labels) */
+#define WCSP_M_MAX 65533          /* largest M of the 16-bit label layout, the fast default */
+#define WCSP_M_MAX_WIDE 2147483646LL   /* largest finite M: budgets in (WCSP_M_MAX, WCSP_M_MAX_WIDE] are not
+                                     an error ("M in R+"; integer f2 makes ceil(M) equivalent) —
+                                     they switch the solve to 32-bit labels and 64-bit stamped temporary
+                                     labels, on the sweep engine (WCSP_ENGINE_PERSISTENT / _STEPPED; a
+                                     wheel-engine handle runs its sweep form for that solve), single device
+                                     only (slab handles and wcsp_staircase return WCSP_EINVAL) */
 
 enum { WCSP_MEM_HOST = 0, WCSP_MEM_DEVICE = 1 };
 enum { WCSP_JUMP = 0,             /* advance t by the min live residual */
@@ -74,7 +80,7 @@ enum { WCSP_HALO_COPY = 0,          /* slab boundary: ghost planes exchanged by 
 /* Problem statement.  Validation (wcsp_create / wcsp_load):
  *  d in 1..4, every shape[k] >= 1, N <= 2^30;  A and B non-empty among the
  *  present vertices and disjoint;  M == WCSP_M_INF or
- *  1 <= M <= WCSP_M_MAX;  every present edge (f1 > 0) has f2 >= 1
+ *  1 <= M <= WCSP_M_MAX_WIDE;  every present edge (f1 > 0) has f2 >= 1
  *  (f : E -> Z_+^2).  Violations return WCSP_EINVAL. */
 typedef struct {
   int32_t d;
@@ -145,6 +151,13 @@ typedef struct {
   int64_t kernel_launches;  /* CUDA kernels this solve launched */
   double device_ms;         /* device time of the solve (init + cycles), CUDA events */
   double cycle_ms;          /* device time of the cycle kernels alone (excludes the init kernel) */
+  int64_t retries;          /* grow-and-rerun attempts after a device-side storage overflow (phantom
+                               pool, event ring, run-descriptor table) */
+  int64_t staging_appended; /* wheel treat: events past the shared-memory staging appended to the
+                               block's open ring regions ... */
+  int64_t staging_spilled;  /* ... past those, written to the block's spill buffer ... */
+  int64_t staging_singles;  /* ... past the spill buffer, filed as runs of one (all exact; counted so
+                               tests can show every path ran) */
 } wcsp_result;
 
 /* One record per cycle when options.trace_cap > 0 (after the cycle ran). */

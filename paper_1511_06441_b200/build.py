@@ -39,7 +39,7 @@ def build(force: bool = False, verbose: bool = False, out: str = SO, defines=())
            out + ".tmp", *SOURCES, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
-    with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
+    with open(out + ".ptxas.log", "w") as f:      # next to the library it describes (untracked)
         f.write(log)
     if res.returncode != 0:
         sys.stderr.write(log)

@@ -83,7 +83,14 @@ struct wcsp_handle {
   unsigned long long* d_cnt = nullptr;               // validation counters
   long long M = 0;
   int nsm = 0, grid = 0;
+  int grid_main = 0;                                 // grid of opt.engine's cycle kernel (grid = this solve's)
   bool big = false;                                  // wheel: the 4-blocks-per-SM cycle kernel
+  // wide labels (M > WCSP_M_MAX): this solve runs the sweep engine on u32 labels + u64 temps
+  int eng = 0;                                       // engine of this solve (opt.engine, or its sweep form)
+  bool wide = false;
+  unsigned* lab = nullptr;                           // [N] u32 labels (allocated on the first wide solve)
+  int pool_rec = 8;                                  // bytes per phantom record in pool[] (16: wide)
+  int grid_wide = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
   long long last_cycles = 0;
   long long launches = 0;
@@ -121,7 +128,9 @@ namespace {
 size_t lane_bytes(int d) { return d <= 2 ? 4 : 8; }
 
 template <int D>
-void* cycle_fn(int engine, bool big) {
+void* cycle_fn(int engine, bool big, bool wide = false) {
+  if (wide) return engine == WCSP_ENGINE_STEPPED ? reinterpret_cast<void*>(&k_sweep<D, true>)
+                                                 : reinterpret_cast<void*>(&k_persistent<D, true>);
   switch (engine) {
     case WCSP_ENGINE_PERSISTENT: return reinterpret_cast<void*>(&k_persistent<D>);
     case WCSP_ENGINE_STEPPED: return reinterpret_cast<void*>(&k_sweep<D>);
@@ -130,9 +139,9 @@ void* cycle_fn(int engine, bool big) {
     default: return reinterpret_cast<void*>(&k_wheel_treat<D>);
   }
 }
-void* cycle_fn_d(int d, int engine, bool big) {
-  return d == 1 ? cycle_fn<1>(engine, big) : d == 2 ? cycle_fn<2>(engine, big) : d == 3 ? cycle_fn<3>(engine, big)
-                                                                                 : cycle_fn<4>(engine, big);
+void* cycle_fn_d(int d, int engine, bool big, bool wide = false) {
+  return d == 1 ? cycle_fn<1>(engine, big, wide) : d == 2 ? cycle_fn<2>(engine, big, wide)
+         : d == 3 ? cycle_fn<3>(engine, big, wide) : cycle_fn<4>(engine, big, wide);
 }
 
 template <int D>
@@ -142,7 +151,9 @@ cudaError_t set_smem_attrs() {
                  reinterpret_cast<void*>(&k_treat<D>), reinterpret_cast<void*>(&k_wheel_persistent<D, 3>),
                  reinterpret_cast<void*>(&k_wheel_persistent<D, 4>),
                  reinterpret_cast<void*>(&k_wheel_fire<D>), reinterpret_cast<void*>(&k_wheel_treat<D>),
-                 reinterpret_cast<void*>(&k_wheel_peer<D, 3>), reinterpret_cast<void*>(&k_wheel_peer<D, 4>)};
+                 reinterpret_cast<void*>(&k_wheel_peer<D, 3>), reinterpret_cast<void*>(&k_wheel_peer<D, 4>),
+                 reinterpret_cast<void*>(&k_persistent<D, true>), reinterpret_cast<void*>(&k_sweep<D, true>),
+                 reinterpret_cast<void*>(&k_treat<D, true>)};
   const char* co = getenv("WCSP_CARVEOUT");       // A/B runs: shared-memory carveout in percent of L1
   for (void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -161,7 +172,7 @@ unsigned win_words_for(unsigned nwords, unsigned nblocks) {
   if (const char* e = getenv("WCSP_WIN_WORDS")) return atoi(e) >= WIN_WORDS ? (unsigned)WIN_WORDS : atoi(e) >= 16 ? 16u : 8u;
   if (nblocks == 0) return 8u;
   const double rounds16 = (double)nwords / (16.0 * nblocks * WARPS);
-  return rounds16 <= 1.0 || rounds16 >= 4.0 ? 16u : 8u;
+  return std::min<unsigned>(rounds16 <= 1.0 || rounds16 >= 4.0 ? 16u : 8u, (unsigned)WIN_WORDS);
 }
 
 Dev make_dev(const wcsp_handle* h) {
@@ -181,6 +192,8 @@ Dev make_dev(const wcsp_handle* h) {
   s.wt = h->wt;
   s.res = h->res;
   s.sw = h->sw;
+  s.lab = h->lab;
+  s.wide = h->wide ? 1 : 0;
   s.tbits = h->tbits;
   s.nwords = h->nwords;
   s.act[0] = h->act[0]; s.act[1] = h->act[1];
@@ -225,14 +238,16 @@ Dev make_dev(const wcsp_handle* h) {
   return s;
 }
 
-wcsp_status alloc_pool(wcsp_handle* h, unsigned long long cap) {
+wcsp_status alloc_pool(wcsp_handle* h, unsigned long long cap, int rec = 0) {
+  if (rec == 0) rec = h->pool_rec;
   if (h->pool[0]) cudaFree(h->pool[0]);
   if (h->pool[1]) cudaFree(h->pool[1]);
   h->pool[0] = h->pool[1] = nullptr;
   h->pool_cap = 0;
-  CK(cudaMalloc(&h->pool[0], cap * sizeof(unsigned long long)));
-  CK(cudaMalloc(&h->pool[1], cap * sizeof(unsigned long long)));
+  CK(cudaMalloc(&h->pool[0], cap * rec));
+  CK(cudaMalloc(&h->pool[1], cap * rec));
   h->pool_cap = cap;
+  h->pool_rec = rec;
   return WCSP_REACHED;
 }
 
@@ -271,10 +286,11 @@ int grid_for(const wcsp_handle* h, unsigned long long n) {
 
 wcsp_status check_M(long long M) {
   if (M == WCSP_M_INF) return WCSP_REACHED;
-  if (M < 1 || M > WCSP_M_MAX)
-    return fail(WCSP_EINVAL, "M = %lld outside [1, %d] (and not WCSP_M_INF)", M, WCSP_M_MAX);
+  if (M < 1 || M > WCSP_M_MAX_WIDE)
+    return fail(WCSP_EINVAL, "M = %lld outside [1, %lld] (and not WCSP_M_INF)", M, (long long)WCSP_M_MAX_WIDE);
   return WCSP_REACHED;
 }
+bool wide_M(long long M) { return M != WCSP_M_INF && M > WCSP_M_MAX; }
 
 wcsp_status validate_device(wcsp_handle* h, const uint8_t* f1, const uint8_t* f2) {
   CK(cudaMemsetAsync(h->d_cnt, 0, 5 * sizeof(unsigned long long), h->stream));
@@ -367,7 +383,7 @@ void release(wcsp_handle* h) {
     delete c;
   }
   h->children.clear();
-  void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->tbits, h->barr,
+  void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->lab, h->tbits, h->barr,
                   h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
                   h->d_cnt, h->d_ghost, h->g_out_lo, h->g_out_hi, h->g_in_lo, h->g_in_hi, h->l_out_lo,
                   h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl, h->spill, h->tlist, h->tcount};
@@ -419,7 +435,7 @@ wcsp_status reset_ctl(wcsp_handle* h) {
   for (int i = 0; i < 3; ++i) c.acc[i].dmin = 0xFFFFFFFFu;
   c.acc[0].tl_over = 1;            // cycle 0 treats A from the bitmap (k_init)
   CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
-  if (is_wheel(h->opt.engine)) {
+  if (is_wheel(h->eng)) {
     CK(cudaMemsetAsync(h->bcounts, 0, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned), h->stream));
     CK(cudaMemsetAsync(h->tcount, 0, (size_t)h->grid * sizeof(unsigned), h->stream));
   }
@@ -439,7 +455,7 @@ wcsp_status launch_init(wcsp_handle* h) {
 wcsp_status run_persistent(wcsp_handle* h) {
   Dev s = make_dev(h);
   void* args[] = {&s};
-  CK(cudaLaunchCooperativeKernel(cycle_fn_d(h->d, h->opt.engine, h->big), dim3(h->grid), dim3(THREADS), args, sizeof(Smem),
+  CK(cudaLaunchCooperativeKernel(cycle_fn_d(h->d, h->eng, h->big, h->wide), dim3(h->grid), dim3(THREADS), args, sizeof(Smem),
                                  h->stream));
   h->launches += 1;
   return WCSP_REACHED;
@@ -448,10 +464,14 @@ wcsp_status run_persistent(wcsp_handle* h) {
 template <int D>
 void launch_cycle(wcsp_handle* h, const Dev& s) {
   const size_t sm = sizeof(Smem);
-  if (is_wheel(h->opt.engine)) {
+  if (is_wheel(h->eng)) {
     k_wheel_fire<D><<<h->grid, THREADS, sm, h->stream>>>(s);
     k_wheel_treat<D><<<h->grid, THREADS, sm, h->stream>>>(s);
     k_wheel_decide<<<1, 32, 0, h->stream>>>(s);
+  } else if (h->wide) {
+    k_sweep<D, true><<<h->grid, THREADS, sm, h->stream>>>(s);
+    k_treat<D, true><<<h->grid, THREADS, sm, h->stream>>>(s);
+    k_decide<<<1, 32, 0, h->stream>>>(s);
   } else {
     k_sweep<D><<<h->grid, THREADS, sm, h->stream>>>(s);
     k_treat<D><<<h->grid, THREADS, sm, h->stream>>>(s);
@@ -477,7 +497,8 @@ wcsp_status run_stepped(wcsp_handle* h) {
     CK(cudaStreamSynchronize(h->stream));
     const int st = h->h_ctl->view.status;
     if (st == ST_WRAP) {               // maintenance pass (stamp wrap / texp refresh), then continue
-      if (is_wheel(h->opt.engine)) k_wheel_maintain<<<h->grid, THREADS, 0, h->stream>>>(s);
+      if (is_wheel(h->eng)) k_wheel_maintain<<<h->grid, THREADS, 0, h->stream>>>(s);
+      else if (h->wide) k_clear_temps<true><<<h->grid, THREADS, 0, h->stream>>>(s);
       else k_clear_temps<<<h->grid, THREADS, 0, h->stream>>>(s);
       h->launches += 1;
       CK(cudaGetLastError());
@@ -509,7 +530,7 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   if ((st = reset_ctl(h)) != WCSP_REACHED) return st;
   if ((st = launch_init(h)) != WCSP_REACHED) return st;
   CK(cudaEventRecord(h->em, h->stream));
-  st = is_stepped(h->opt.engine) ? run_stepped(h) : run_persistent(h);
+  st = is_stepped(h->eng) ? run_stepped(h) : run_persistent(h);
   if (st != WCSP_REACHED) return st;
   CK(cudaEventRecord(h->e1, h->stream));
   CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
@@ -537,29 +558,81 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   r->lanes_started = c.started;
   r->peak_active = c.peak_active;
   r->peak_phantoms = c.peak_phantoms;
-  r->phantom_capacity = (long long)(is_wheel(h->opt.engine) ? h->ev_cap : h->pool_cap);
+  r->phantom_capacity = (long long)(is_wheel(h->eng) ? h->ev_cap : h->pool_cap);
   r->kernel_launches = h->launches;
   r->device_ms = ms;
   r->cycle_ms = cms;
+  r->staging_appended = (long long)c.n_appended;
+  r->staging_spilled = (long long)c.n_spilled;
+  r->staging_singles = (long long)c.n_single;
   h->last_cycles = c.cycles;
   if (*status == WCSP_EOVERFLOW) r->phantom_capacity = c.need_pool;
   return WCSP_REACHED;
 }
 
+// Device-side overflow path ("difficulties with dynamic memory locations"): a
+// storage overflow ends the run with a flag and the needed size; the host grows exactly the
+// structure that overflowed and re-runs.  The size a run reports is only what its failing cycle
+// needed (the front keeps growing), so a retry takes twice that and at least 4x the old size
+// (2x once the structure is past 2^26 entries, where memory matters).
+constexpr int MAX_ATTEMPTS = 12;
+unsigned long long grown(unsigned long long cap, long long need) {
+  const unsigned long long f = cap < (1ull << 26) ? 4 : 2;
+  return std::max<unsigned long long>(2ull * (unsigned long long)std::max(need, 0ll), f * cap);
+}
+
+// Budgets above WCSP_M_MAX run the sweep engine with u32 labels and u64 stamped temps
+// (include/wcsp.h; the 16-bit layout stays the default): allocate its state on first use.
+wcsp_status prepare_engine(wcsp_handle* h) {
+  h->wide = wide_M(h->M);
+  if (!h->wide) {
+    h->eng = h->opt.engine;
+    h->grid = h->grid_main;
+    return WCSP_REACHED;
+  }
+  h->eng = is_stepped(h->opt.engine) ? WCSP_ENGINE_STEPPED : WCSP_ENGINE_PERSISTENT;
+  const unsigned long long N = h->N;
+  if (!h->lab) CK(cudaMalloc(&h->lab, N * sizeof(unsigned)));
+  if (!h->res) CK(cudaMalloc(&h->res, N * lane_bytes(h->d)));
+  if (!h->act[0]) CK(cudaMalloc(&h->act[0], N * sizeof(unsigned)));
+  if (!h->act[1]) CK(cudaMalloc(&h->act[1], N * sizeof(unsigned)));
+  if (!h->pool[0] || h->pool_rec != (int)sizeof(PhW)) {
+    const unsigned long long cap = h->opt.phantom_capacity > 0 ? (unsigned long long)h->opt.phantom_capacity
+                                                               : std::max<unsigned long long>(4 * N, 1ull << 20);
+    wcsp_status st = alloc_pool(h, cap, (int)sizeof(PhW));
+    if (st != WCSP_REACHED) return st;
+  }
+  if (!h->grid_wide) {
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_fn_d(h->d, h->eng, false, true), THREADS,
+                                                     sizeof(Smem)));
+    if (per_sm < 1) return fail(WCSP_ECUDA, "wide cycle kernel cannot be resident");
+    h->grid_wide = std::min(per_sm * h->nsm, h->grid_main);
+  }
+  h->grid = h->grid_wide;
+  return WCSP_REACHED;
+}
+
 wcsp_status solve_impl(wcsp_handle* h, wcsp_result* out) {
+  {
+    wcsp_status st = prepare_engine(h);
+    if (st != WCSP_REACHED) return st;
+  }
   wcsp_result r;
   int status = ST_RUNNING;
-  for (int attempt = 0; attempt < 6; ++attempt) {
+  int attempt = 0;
+  for (; attempt < MAX_ATTEMPTS; ++attempt) {
     wcsp_status st = solve_once(h, &r, &status);
     if (st != WCSP_REACHED) return st;
+    r.retries = attempt;
     if (status != WCSP_EOVERFLOW) break;
     // overflow of a device structure: grow it and re-run (device flag -> host retry)
     const long long need = r.phantom_capacity;
-    if (is_wheel(h->opt.engine)) {
+    if (is_wheel(h->eng)) {
       if (need == -2) st = alloc_desc(h, h->dcap * 2);
-      else st = alloc_ring(h, std::max<unsigned long long>((unsigned long long)need + need / 2, h->ev_cap * 2));
+      else st = alloc_ring(h, grown(h->ev_cap, need));
     } else {
-      st = alloc_pool(h, std::max<unsigned long long>((unsigned long long)need + need / 2, h->pool_cap * 2));
+      st = alloc_pool(h, grown(h->pool_cap, need));
     }
     if (st != WCSP_REACHED) return st;
   }
@@ -627,7 +700,8 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
   if (per_sm < 1) CKH(fail(WCSP_ECUDA, "cycle kernel cannot be resident"));
   if (bps) per_sm = std::max(1, std::min(per_sm, atoi(bps)));
   if (spec && spec->per_sm > 0) per_sm = spec->per_sm;     // peer-halo slab: sized for the peer kernel
-  h->grid = per_sm * h->nsm;
+  h->grid = h->grid_main = per_sm * h->nsm;
+  h->eng = opt.engine;
   const size_t fb = (size_t)h->d * N;
   CKC(cudaMalloc(&h->d_f1, fb));
   CKC(cudaMalloc(&h->d_f2, fb));
@@ -647,8 +721,12 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
   const unsigned long long cap = opt.phantom_capacity > 0 ? (unsigned long long)opt.phantom_capacity
                                                           : std::max<unsigned long long>(4 * N, 1ull << 20);
   if (is_wheel(opt.engine)) {
-    CKH(alloc_ring(h, std::max<unsigned long long>(opt.phantom_capacity > 0 ? cap : 2 * cap, (unsigned long long)h->grid * 2 * 4096)));
-    CKH(alloc_desc(h, 32));
+    // auto: twice the sweep pool's default and room for every block's open regions; an explicit
+    // capacity is taken as given (the overflow path grows it)
+    CKH(alloc_ring(h, opt.phantom_capacity > 0 ? cap
+                                               : std::max<unsigned long long>(2 * cap, (unsigned long long)h->grid * 2 * 4096)));
+    const char* dc = getenv("WCSP_DCAP");          // tests: a tiny run-descriptor table forces its overflow path
+    CKH(alloc_desc(h, dc ? (unsigned)std::max(1, atoi(dc)) : 32u));
     CKC(cudaMalloc(&h->bcounts, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned)));
     // spill room per block and flush period: a dense window round (e.g. the initial treatment
     // of a whole boundary) can stage several times the shared-memory staging
@@ -770,6 +848,7 @@ wcsp_status peer_connect(wcsp_handle* g);
 wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_handle** out) {
   if (p->mem != WCSP_MEM_HOST) return fail(WCSP_EINVAL, "the slab engine takes host arrays");
   if (!is_wheel(opt.engine)) return fail(WCSP_EINVAL, "the slab engine runs the wheel engine (engine = WHEEL)");
+  if (wide_M(p->M)) return fail(WCSP_EINVAL, "slab engine: M > %d (wide labels) is single-device only", WCSP_M_MAX);
   const bool dist = opt.nccl_id != nullptr && opt.nranks >= 1;   // nranks = 1: NCCL path on one GPU (tests)
   if (dist && (opt.rank < 0 || opt.rank >= opt.nranks || !opt.nccl_id))
     return fail(WCSP_EINVAL, "multi-GPU slab engine needs 0 <= rank < nranks and nccl_id");
@@ -1007,6 +1086,9 @@ wcsp_status group_collect(wcsp_handle* g, wcsp_result* r, int* status) {
     r->relabels += cs[i].relabels;
     r->lanes_started += cs[i].started;
     r->peak_phantoms += cs[i].peak_phantoms;
+    r->staging_appended += (long long)cs[i].n_appended;
+    r->staging_spilled += (long long)cs[i].n_spilled;
+    r->staging_singles += (long long)cs[i].n_single;
     ch[i]->last_cycles = cs[i].cycles;
     if (cs[i].need_pool) need = cs[i].need_pool == -2 ? -2 : std::max(need, cs[i].need_pool);
     if (cs[i].abort) return fail(WCSP_ECUDA, "slab %d: barrier watchdog fired", i);
@@ -1130,8 +1212,8 @@ wcsp_status dist_collect(wcsp_handle* g, wcsp_result* r, int* status) {
   Ctl cs;
   CK(cudaMemcpyAsync(&cs, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
   CK(cudaStreamSynchronize(g->stream));
-  long long sums[8] = {cs.edge_updates, cs.arrivals, cs.triggered, cs.created, cs.relabels, cs.started,
-                       cs.peak_phantoms, 0};
+  long long sums[10] = {cs.edge_updates, cs.arrivals, cs.triggered, cs.created, cs.relabels, cs.started,
+                        cs.peak_phantoms, (long long)cs.n_appended, (long long)cs.n_spilled, (long long)cs.n_single};
   unsigned long long mins[2] = {cs.ybest, 0}, maxs[2] = {(unsigned long long)std::max(0ll, cs.need_pool),
                                                          cs.need_pool == -2 ? 1ull : 0ull};
   long long* dsum = nullptr;
@@ -1142,7 +1224,7 @@ wcsp_status dist_collect(wcsp_handle* g, wcsp_result* r, int* status) {
   CK(cudaMemcpyAsync(dsum, sums, sizeof(sums), cudaMemcpyHostToDevice, g->stream));
   CK(cudaMemcpyAsync(dmin, mins, sizeof(mins), cudaMemcpyHostToDevice, g->stream));
   CK(cudaMemcpyAsync(dmax, maxs, sizeof(maxs), cudaMemcpyHostToDevice, g->stream));
-  NCK(nc.allReduce(dsum, dsum, 8, ncclInt64, ncclSum, comm, g->stream));
+  NCK(nc.allReduce(dsum, dsum, 10, ncclInt64, ncclSum, comm, g->stream));
   NCK(nc.allReduce(dmin, dmin, 2, ncclUint64, ncclMin, comm, g->stream));
   NCK(nc.allReduce(dmax, dmax, 2, ncclUint64, ncclMax, comm, g->stream));
   CK(cudaMemcpyAsync(sums, dsum, sizeof(sums), cudaMemcpyDeviceToHost, g->stream));
@@ -1157,6 +1239,7 @@ wcsp_status dist_collect(wcsp_handle* g, wcsp_result* r, int* status) {
   memset(r, 0, sizeof(*r));
   r->edge_updates = sums[0]; r->arrivals = sums[1]; r->triggered = sums[2]; r->phantoms_created = sums[3];
   r->relabels = sums[4]; r->lanes_started = sums[5]; r->peak_phantoms = sums[6];
+  r->staging_appended = sums[7]; r->staging_spilled = sums[8]; r->staging_singles = sums[9];
   r->cycles = cs.cycles;
   c->last_cycles = g->last_cycles = cs.cycles;
   if (*status == WCSP_REACHED) {
@@ -1327,14 +1410,20 @@ wcsp_status peer_connect(wcsp_handle* g) {
 wcsp_status group_solve(wcsp_handle* g, wcsp_result* out) {
   wcsp_result r;
   int status = ST_RUNNING;
-  for (int attempt = 0; attempt < 6; ++attempt) {
+  for (int attempt = 0; attempt < MAX_ATTEMPTS; ++attempt) {
     wcsp_status st = g->halo == WCSP_HALO_PEER ? peer_solve_once(g, &r, &status)
                    : g->comm ? dist_solve_once(g, &r, &status) : group_solve_once(g, &r, &status);
     if (st != WCSP_REACHED) return st;
+    r.retries = attempt;
     if (status != WCSP_EOVERFLOW) break;
-    for (auto* c : g->children) {     // grow every child's wheel storage and re-run
-      if ((st = alloc_desc(c, c->dcap * 2)) != WCSP_REACHED) return st;
-      if ((st = alloc_ring(c, c->ev_cap * 2)) != WCSP_REACHED) return st;
+    // grow what overflowed in every slab (same sizes everywhere: the peer kernel's slabs and
+    // the ranks share one layout) and re-run: -2 = the run-descriptor table, else the ring
+    // slots the largest slab needed
+    const long long need = r.phantom_capacity;
+    for (auto* c : g->children) {
+      if (need == -2) st = alloc_desc(c, c->dcap * 2);
+      else st = alloc_ring(c, grown(c->ev_cap, need));
+      if (st != WCSP_REACHED) return st;
     }
   }
   if (status == WCSP_EOVERFLOW) return fail(WCSP_EOVERFLOW, "event storage overflow after retries");
@@ -1401,6 +1490,7 @@ wcsp_status wcsp_set_targets(wcsp_handle* h, const uint8_t* maskB, const uint8_t
   if ((st = check_M(M)) != WCSP_REACHED) return st;
   if (!h->children.empty()) {
     if (maskB || present || present_all) return fail(WCSP_EINVAL, "slab handles only change M");
+    if (wide_M(M)) return fail(WCSP_EINVAL, "slab engine: M > %d (wide labels) is single-device only", WCSP_M_MAX);
     h->M = M;
     return WCSP_REACHED;
   }
@@ -1554,6 +1644,8 @@ wcsp_status wcsp_staircase(wcsp_handle* h, int64_t M_max, int64_t f2_stop, int64
     return fail(WCSP_EINVAL, "wcsp_staircase needs a single-device wheel-engine handle");
   wcsp_status st;
   if ((st = check_M(M_max)) != WCSP_REACHED) return st;
+  if (wide_M(M_max)) return fail(WCSP_EINVAL, "wcsp_staircase: M_max > %d needs the wide-label sweep engine "
+                                               "(the staircase runs on the 16-bit wheel engine)", WCSP_M_MAX);
   CK(cudaSetDevice(h->dev));
   const unsigned want = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, 1 << 24));
   if (want > h->stair_cap) {

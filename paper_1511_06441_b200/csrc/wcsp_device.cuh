@@ -30,6 +30,7 @@
 // overwrites, so an arrival learns what D is from the atomic's return value.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace wcspk {
@@ -60,6 +61,15 @@ constexpr unsigned TMP_B = 0xFFFF0001u;    // temp sentinel of a target vertex
 constexpr unsigned TMP_REMOVED = 0xFFFF0000u;
 constexpr unsigned TMP_GHOST = 0xFFFF0002u;    // slab engine: a neighbouring slab's boundary vertex
 constexpr unsigned TMP_GHOST_B = 0xFFFF0003u;  // ... that is a target
+// Wide labels (budgets M > WCSP_M_MAX, include/wcsp.h; sweep engine only): label L(v) is a u32 in
+// Dev::lab, the state word sw[v] holds only temp = stamp:32 | cand:32 (64-bit atomicMax); sentinel
+// stamp 0xFFFFFFFF as in the 16-bit layout.  Phantom records are 16 bytes (see PhW).
+constexpr unsigned LBL_REMOVED_W = 0x7FFFFFFFu;   // > any cand (M <= 2^31 - 2): no S6 test passes
+constexpr unsigned long long TMPW_SENT = 0xFFFFFFFFull << 32;
+constexpr unsigned long long TMPW_REMOVED = TMPW_SENT | 0ull;
+constexpr unsigned long long TMPW_B = TMPW_SENT | 1ull;
+struct __align__(16) PhW { unsigned long long x, y; };   // x: src 30 | lane 3 | res 8 (bit 33); y: cand
+constexpr int PHW_RES = 33;
 constexpr int ST_RUNNING = -1;
 constexpr int ST_WRAP = 100;               // stepped engines: maintenance pass needed (host launches it)
 
@@ -116,6 +126,10 @@ struct Ctl {
   unsigned long long ybest;        // (src << 1 | via) of the best arrival at X seen by this slab
   unsigned n_stair, pad3_;         // staircase steps recorded
   long long stair_q;               // best target quality so far
+  long long prop_need;             // peer halo: ring slots the leader's proposal asked for (with prop)
+  unsigned long long n_appended;   // wheel treat: events past the shared staging appended to open regions
+  unsigned long long n_spilled;    // ... past those, written to the block's spill buffer
+  unsigned long long n_single;     // ... past the spill buffer, filed as runs of one
   alignas(128) unsigned long long grel;   // grid barrier: the last block to arrive releases this target
   unsigned long long pad4_[15];           // (its own 128-byte line: pollers do not slow the arrivals)
   alignas(128) unsigned long long bsub[WCSP_BAR_GROUPS][16];   // WCSP_BAR_GROUPS > 1: per-group arrivals
@@ -133,7 +147,9 @@ struct Dev {
   unsigned off[8];                 // lane 2k: +stride_k, lane 2k+1: -stride_k (mod 2^32)
   const void* wt;                  // weight records (f1 lane word, f2 lane word) per vertex
   void* res;                       // sweep engine: lane residual words, 0 = idle lane
-  unsigned long long* sw;          // vertex state words (label | temp)
+  unsigned long long* sw;          // vertex state words (label | temp); wide: temp only
+  unsigned* lab;                   // wide labels (M > WCSP_M_MAX): L(v) as u32
+  int wide;
   unsigned* tbits;                 // triggered bitmap (first arrivals of the cycle)
   unsigned nwords;                 // words of the bitmap
   unsigned win_words;              // bitmap words per warp window of the treat (8 or 16)
@@ -397,11 +413,15 @@ __device__ __forceinline__ void qpush(T* qbuf, unsigned qcap, unsigned* qn, bool
   }
 }
 
-// Flush the active-list and phantom queues with one reservation round.
-__device__ __forceinline__ void qflush(Smem& sm, unsigned* ga, unsigned* outa, unsigned* gp, unsigned long long* outp,
+// Flush the active-list and phantom queues with one reservation round (P: the phantom record,
+// u64 or the wide layout's PhW staged in the same shared buffer).
+template <class P = unsigned long long>
+__device__ __forceinline__ void qflush(Smem& sm, unsigned* ga, unsigned* outa, unsigned* gp, P* outp,
                                        unsigned long long capp) {
+  constexpr unsigned QCAP = QP_CAP * sizeof(unsigned long long) / sizeof(P);
+  const P* qp = reinterpret_cast<const P*>(sm.qp);
   __syncthreads();
-  const unsigned na = min(sm.na, (unsigned)QA_CAP), np = min(sm.np, (unsigned)QP_CAP);
+  const unsigned na = min(sm.na, (unsigned)QA_CAP), np = min(sm.np, QCAP);
   if (na == 0 && np == 0) return;                 // uniform: every thread read the same counts
   if (threadIdx.x == 0) {
     sm.base_a = na ? atomicAdd(ga, na) : 0u;
@@ -411,7 +431,7 @@ __device__ __forceinline__ void qflush(Smem& sm, unsigned* ga, unsigned* outa, u
   const unsigned long long ba = sm.base_a, bb = sm.base_b;
   for (unsigned i = threadIdx.x; i < na; i += THREADS) outa[ba + i] = sm.qa[i];
   for (unsigned i = threadIdx.x; i < np; i += THREADS)
-    if (bb + i < capp) outp[bb + i] = sm.qp[i];
+    if (bb + i < capp) outp[bb + i] = qp[i];
   if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; }  // no push can happen before the barrier below
   __syncthreads();
 }
@@ -548,10 +568,43 @@ __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* ac
   }
 }
 
+// The same two halves for wide labels: temp(D) = stamp:32 | cand:32, one 64-bit atomicMax.
+__device__ __forceinline__ unsigned long long arrive_atomic_w(const Dev& s, const View& v, bool go, unsigned D,
+                                                              int cand) {
+  const unsigned long long key = ((unsigned long long)v.stamp << 32) | (unsigned)cand;
+  return go ? atomicMax(s.sw + D, key) : key;
+}
+__device__ __forceinline__ void arrive_post_w(const Dev& s, const View& v, Acc* acc, unsigned long long old,
+                                              unsigned D, int cand, unsigned src, unsigned via) {
+  const unsigned os = (unsigned)(old >> 32);
+  if (os == 0xFFFFFFFFu) {
+    if (old == TMPW_B) {           // termination 1°
+      const unsigned Dg = D + s.goff;
+      atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - Dg));
+      const unsigned k = atomicAdd(&s.ctl->n_barr, 1u);
+      if (k < s.barr_cap) s.barr[k] = BArr{Dg, (unsigned)cand, src, via};
+    }
+  } else if (os != v.stamp) {      // first arrival of the cycle
+    atomicOr(s.tbits + (D >> 5), 1u << (D & 31u));
+  }
+}
+template <bool W> using OldT = std::conditional_t<W, unsigned long long, unsigned>;
+template <bool W>
+__device__ __forceinline__ OldT<W> arrive_a(const Dev& s, const View& v, bool go, unsigned D, int cand) {
+  if constexpr (W) return arrive_atomic_w(s, v, go, D, cand);
+  else return arrive_atomic(s, v, go, D, cand);
+}
+template <bool W>
+__device__ __forceinline__ void arrive_p(const Dev& s, const View& v, Acc* acc, OldT<W> old, unsigned D, int cand,
+                                         unsigned src, unsigned via) {
+  if constexpr (W) arrive_post_w(s, v, acc, old, D, cand, src, via);
+  else arrive_post(s, v, acc, old, D, cand, src, via);
+}
+
 // ---------------------------------------------------------------------------
 // sweep: Steps 1, 3, 7 and the retirement part of 8-9 (sweep engine)
 // ---------------------------------------------------------------------------
-template <int D>
+template <int D, bool W = false>
 __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
   using LW = typename Tr<D>::LW;
   Acc* acc = &s.ctl->acc[v.c % 3];
@@ -599,26 +652,62 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
       for (int it = 0; it < SWEEP_ITEMS; ++it) {
         lbl[it] = 0; f2w[it] = 0;
         if (fired[it]) {
-          lbl[it] = s.minf ? 1u : (__ldcg(lbl_ptr(s.sw, vx[it])) & 0xFFFFu);
+          if constexpr (W) lbl[it] = s.minf ? 1u : __ldcg(s.lab + vx[it]);
+          else lbl[it] = s.minf ? 1u : (__ldcg(lbl_ptr(s.sw, vx[it])) & 0xFFFFu);
           if (!s.minf) f2w[it] = load_f2<D>(s, vx[it]);
         }
       }
 #pragma unroll
       for (int it = 0; it < SWEEP_ITEMS; ++it) {
         if (!fired[it]) continue;
-        unsigned old[2 * D];
+        OldT<W> old[2 * D];
 #pragma unroll
         for (int j = 0; j < 2 * D; ++j) {
           const bool fj = (fired[it] >> (8 * j + 7)) & 1;
           arr += fj;
           const int cand = (int)lbl[it] - (int)((f2w[it] >> (8 * j)) & 0xFF);
-          old[j] = arrive_atomic(s, v, fj && cand > 0, vx[it] + s.off[j], cand);
+          old[j] = arrive_a<W>(s, v, fj && cand > 0, vx[it] + s.off[j], cand);
         }
 #pragma unroll
         for (int j = 0; j < 2 * D; ++j) {
           const int cand = (int)lbl[it] - (int)((f2w[it] >> (8 * j)) & 0xFF);
-          arrive_post(s, v, acc, old[j], vx[it] + s.off[j], cand, vx[it] + s.goff, 0u);
+          arrive_p<W>(s, v, acc, old[j], vx[it] + s.off[j], cand, vx[it] + s.goff, 0u);
         }
+      }
+    } else if constexpr (W) {        // wide phantoms: 16-byte records, 64-bit temp atomics
+      const unsigned pc = ch - na_ch;
+      const PhW* pin = reinterpret_cast<const PhW*>(pool_in);
+      PhW* pout = reinterpret_cast<PhW*>(pool_out);
+      PhW p[SWEEP_ITEMS];
+#pragma unroll
+      for (int it = 0; it < SWEEP_ITEMS; ++it) {
+        const unsigned i = pc * chunk + it * THREADS + threadIdx.x;
+        if ((unsigned)it < items && i < v.n_pool) {
+          const ulonglong2 q2 = __ldcs(reinterpret_cast<const ulonglong2*>(pin + i));
+          p[it] = PhW{q2.x, q2.y};
+        } else {
+          p[it] = PhW{0ull, 0ull};
+        }
+      }
+      unsigned long long old[SWEEP_ITEMS];
+#pragma unroll
+      for (int it = 0; it < SWEEP_ITEMS; ++it) {
+        const unsigned r = (unsigned)(p[it].x >> PHW_RES) & 0xFFu;   // 0 only for padding
+        const bool fire = r != 0 && r == v.delta;
+        const bool keep = r > v.delta;
+        if (keep) dmin = min(dmin, r - v.delta);
+        arr += fire;
+        qpush<PhW>(reinterpret_cast<PhW*>(sm.qp), QP_CAP / 2, &sm.np, keep,
+                   PhW{p[it].x - ((unsigned long long)v.delta << PHW_RES), p[it].y}, &acc->n_pool, pout, s.pool_cap);
+        const unsigned src = (unsigned)p[it].x & 0x3FFFFFFFu;
+        const unsigned lane = (unsigned)(p[it].x >> PH_LANE) & 7u;
+        old[it] = arrive_atomic_w(s, v, fire, src + s.off[lane], (int)(unsigned)p[it].y);
+      }
+#pragma unroll
+      for (int it = 0; it < SWEEP_ITEMS; ++it) {
+        const unsigned src = (unsigned)p[it].x & 0x3FFFFFFFu;
+        const unsigned lane = (unsigned)(p[it].x >> PH_LANE) & 7u;
+        arrive_post_w(s, v, acc, old[it], src + s.off[lane], (int)(unsigned)p[it].y, src + s.goff, 1u);
       }
     } else {
       const unsigned pc = ch - na_ch;
@@ -649,7 +738,8 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
         arrive_post(s, v, acc, old[it], src + s.off[lane], (int)((p[it] >> PH_CAND) & 0xFFFFu), src + s.goff, 1u);
       }
     }
-    qflush(sm, &acc->n_act, act_out, &acc->n_pool, pool_out, s.pool_cap);
+    if constexpr (W) qflush<PhW>(sm, &acc->n_act, act_out, &acc->n_pool, reinterpret_cast<PhW*>(pool_out), s.pool_cap);
+    else qflush(sm, &acc->n_act, act_out, &acc->n_pool, pool_out, s.pool_cap);
   }
   block_reduce_commit(sm, dmin, live, arr, 0, 0, 0, acc);
 }
@@ -740,7 +830,7 @@ __device__ __forceinline__ void window_emit(const Dev& s, unsigned bits, unsigne
 // WHEEL = false: lanes are residual bytes in res[q]; phantoms go to the pool.
 // WHEEL = true : lanes and phantoms are events filed at t + f1 (wcsp_wheel.cuh).
 // ---------------------------------------------------------------------------
-template <int D, bool WHEEL_ENGINE, bool PEER = false>
+template <int D, bool WHEEL_ENGINE, bool PEER = false, bool W = false>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
                                           unsigned& dmin, unsigned& created,
                                           unsigned& relabels, unsigned& triggered,
@@ -778,7 +868,7 @@ __device__ void ev_push_warp(const Dev& s, Smem& sm, bool pred, unsigned long lo
 __device__ void warp_flush(const Dev& s, Smem& sm, long long t, unsigned region);
 __device__ void regions_close(const Dev& s, Smem& sm, long long t);
 
-template <int D, bool WHEEL_ENGINE, bool PEER>
+template <int D, bool WHEEL_ENGINE, bool PEER, bool W>
 __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm, Acc* acc, unsigned q,
                                           unsigned& dmin, unsigned& created,
                                           unsigned& relabels, unsigned& triggered,
@@ -786,6 +876,53 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
   using LW = typename Tr<D>::LW;
   const bool valid = q != 0xFFFFFFFFu;
   tested += valid;
+  if constexpr (W) {
+    static_assert(!WHEEL_ENGINE && !PEER, "wide labels: sweep engine, single device");
+    // Wide labels: the same Steps 4, 5, 8.1 on L(v) = lab[v] (u32) and temp = stamp:32 | cand:32
+    const unsigned long long tq = valid ? __ldcg(s.sw + q) : 0ull;
+    const int lq = valid ? (int)__ldcg(s.lab + q) : 0;
+    const WRec<LW> wr = valid ? load_wt_cs<D>(s, q) : WRec<LW>{0, 0};
+    const LW w = valid ? __ldcg(reinterpret_cast<LW*>(s.res) + q) : (LW)0;
+    const int lstar = (int)(unsigned)tq;                         // L* = temp(Q) (reading R23)
+    const bool trig = valid && lstar > lq;
+    const bool inactive = trig && w == 0;                        // reading R6
+    triggered += trig;
+    int rl[2 * D];
+    unsigned long long rtw[2 * D];
+#pragma unroll
+    for (int j = 0; j < 2 * D; ++j) {
+      const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
+      const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
+      const bool test = trig && f1j != 0 && lstar - (int)f2j > 0;
+      rl[j] = test ? (int)__ldcg(s.lab + q + s.off[j]) : (int)LBL_REMOVED_W;
+      rtw[j] = test ? __ldcg(s.sw + q + s.off[j]) : 0ull;
+    }
+    LW neww = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * D; ++j) {
+      const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
+      const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
+      const int c = lstar - (int)f2j;
+      const int rt = (unsigned)(rtw[j] >> 32) == v.stamp ? (int)(unsigned)rtw[j] : 0;
+      const bool pass = c > max(rl[j], rt);                      // edge triggered
+      const bool ph = pass && !inactive;                         // phantom
+      created += ph;
+      lanes_started += pass && inactive;                         // time restored to f1
+      if (pass) dmin = min(dmin, f1j);
+      if (pass && inactive) neww |= (LW)f1j << (8 * j);
+      const PhW prec{(unsigned long long)q | ((unsigned long long)j << PH_LANE) | ((unsigned long long)f1j << PHW_RES),
+                     (unsigned long long)(unsigned)c};
+      qpush<PhW>(reinterpret_cast<PhW*>(sm.qp), QP_CAP / 2, &sm.np, ph, prec, &acc->n_pool,
+                 reinterpret_cast<PhW*>(s.pool[v.cur ^ 1]), s.pool_cap);
+    }
+    if (inactive) {                                              // Step 8.1
+      relabels += 1;
+      s.lab[q] = (unsigned)lstar;
+      if (neww) __stcg(reinterpret_cast<LW*>(s.res) + q, neww);
+    }
+    qpush<unsigned>(sm.qa, QA_CAP, &sm.na, inactive && neww != 0, q, &acc->n_act, s.act[v.cur ^ 1], 0xFFFFFFFFull);
+    return;
+  }
   const unsigned long long swq = valid ? ld_hint(s.sw + q, pol_last()) : 0ull;
   const WRec<LW> wr = valid ? load_wt_cs<D>(s, q) : WRec<LW>{0, 0};
   unsigned long long swr[2 * D];
@@ -918,7 +1055,7 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
 // Flush hook of the wheel (defined in wcsp_wheel.cuh).
 __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, bool final_flush);
 
-template <int D, bool WHEEL_ENGINE, bool PEER = false>
+template <int D, bool WHEEL_ENGINE, bool PEER = false, bool W = false>
 __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   Acc* acc = &s.ctl->acc[v.c % 3];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
@@ -1003,7 +1140,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
       const unsigned q = b + lane < total ? win * s.win_words * 32u + sm.wl[warp][b + lane] : 0xFFFFFFFFu;
-      treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
+      treat_one<D, WHEEL_ENGINE, PEER, W>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
     }
     if constexpr (WHEEL_ENGINE) {
 #if WCSP_WARP_FLUSH
@@ -1014,7 +1151,11 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
 #elif WCSP_FLUSH_LAZY == 0
       ev_flush(s, sm, v.t, v.region, false);
 #endif                             // < 0: no block barrier between rounds; overflow spills, one flush at the end
-    } else qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
+    } else if constexpr (W) {
+      qflush<PhW>(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, reinterpret_cast<PhW*>(s.pool[v.cur ^ 1]), s.pool_cap);
+    } else {
+      qflush(sm, &acc->n_act, s.act[v.cur ^ 1], &acc->n_pool, s.pool[v.cur ^ 1], s.pool_cap);
+    }
   }
   if constexpr (WHEEL_ENGINE) {
 #if WCSP_WARP_FLUSH
@@ -1197,18 +1338,23 @@ __device__ __forceinline__ void init_smem(Smem& sm) {
 
 // Forget every temp (keeps the target / removed sentinels): used when the
 // 16-bit cycle stamps wrap.
+template <bool W = false>
 __device__ __forceinline__ void clear_temps(const Dev& s) {
   for (unsigned long long i = (unsigned long long)blockIdx.x * THREADS + threadIdx.x; i < s.N;
        i += (unsigned long long)gridDim.x * THREADS) {
-    unsigned* t = tmp_ptr(s.sw, (unsigned)i);
-    if ((*t >> 16) != 0xFFFFu) *t = 0u;
+    if constexpr (W) {
+      if ((s.sw[i] >> 32) != 0xFFFFFFFFull) s.sw[i] = 0ull;
+    } else {
+      unsigned* t = tmp_ptr(s.sw, (unsigned)i);
+      if ((*t >> 16) != 0xFFFFu) *t = 0u;
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // kernels (sweep engine)
 // ---------------------------------------------------------------------------
-template <int D>
+template <int D, bool W = false>   // W: wide labels (M > WCSP_M_MAX)
 __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_persistent(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
@@ -1222,7 +1368,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_persistent(Dev s) 
         reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
         s.ctl->ts0 = globaltimer_ns();
       }
-      phase_sweep<D>(s, v, sm);
+      phase_sweep<D, W>(s, v, sm);
       target += G;
       if (!grid_sync(s.ctl, target, sm)) return;
     }
@@ -1232,7 +1378,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_persistent(Dev s) 
     const unsigned long long bhit = sm.bhit;
     __syncthreads();
     if (!bhit) {                                   // S5 precedes S6: the final cycle skips the treat
-      phase_treat<D, false>(s, v, sm);
+      phase_treat<D, false, false, W>(s, v, sm);
       target += G;
       if (!grid_sync(s.ctl, target, sm)) return;
     }
@@ -1245,14 +1391,14 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_persistent(Dev s) 
     v = sm.view;
     __syncthreads();
     if (v.status == ST_RUNNING && v.stamp == 1u) { // stamps wrapped: forget every temp (rare)
-      clear_temps(s);
+      clear_temps<W>(s);
       target += G;
       if (!grid_sync(s.ctl, target, sm)) return;
     }
   }
 }
 
-template <int D>
+template <int D, bool W = false>
 __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_sweep(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
@@ -1263,10 +1409,10 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_sweep(Dev s) {
     reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
     s.ctl->ts0 = globaltimer_ns();
   }
-  phase_sweep<D>(s, v, sm);
+  phase_sweep<D, W>(s, v, sm);
 }
 
-template <int D>
+template <int D, bool W = false>
 __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_treat(Dev s) {
   Smem& sm = smem();
   init_smem(sm);
@@ -1275,7 +1421,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_treat(Dev s) {
   if (v.status != ST_RUNNING) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
   if (__ldcg(&s.ctl->acc[v.c % 3].bhit)) return;
-  phase_treat<D, false>(s, v, sm);
+  phase_treat<D, false, false, W>(s, v, sm);
 }
 
 __global__ void k_decide(Dev s) {
@@ -1286,7 +1432,8 @@ __global__ void k_decide(Dev s) {
   if (v.status == ST_RUNNING && v.stamp == 1u) s.ctl->view.status = ST_WRAP;
 }
 
-__global__ void __launch_bounds__(THREADS) k_clear_temps(Dev s) { clear_temps(s); }
+template <bool W = false>
+__global__ void __launch_bounds__(THREADS) k_clear_temps(Dev s) { clear_temps<W>(s); }
 
 // Initial state (reading R20): L = 0 everywhere, target /
 // removed sentinels, no live lane, A triggered with temp M (the treat of
@@ -1300,12 +1447,17 @@ __global__ void __launch_bounds__(THREADS) k_init(Dev s, const uint8_t* maskA, c
     const bool p = present ? present[i] != 0 : true;
     const bool a = p && maskA[i] && !(ghost && ghost[i]);
     const bool b = p && maskB[i];
-    unsigned lbl = 0, tmp = 0;
-    if (!p) { lbl = LBL_REMOVED; tmp = TMP_REMOVED; }
-    else if (ghost && ghost[i]) { lbl = 0; tmp = ghost[i] == 2 ? TMP_GHOST_B : TMP_GHOST; }   // slab engine
-    else if (b) { lbl = 0; tmp = TMP_B; }
-    else if (a) { lbl = 0; tmp = (stamp_of(0) << 16) | (unsigned)lblA; }
-    s.sw[i] = ((unsigned long long)tmp << 32) | lbl;
+    if (s.wide) {                   // wide labels: L in lab[], temp = stamp:32 | cand:32 in sw[]
+      s.lab[i] = p ? 0u : LBL_REMOVED_W;
+      s.sw[i] = !p ? TMPW_REMOVED : b ? TMPW_B : a ? (((unsigned long long)stamp_of(0) << 32) | (unsigned)lblA) : 0ull;
+    } else {
+      unsigned lbl = 0, tmp = 0;
+      if (!p) { lbl = LBL_REMOVED; tmp = TMP_REMOVED; }
+      else if (ghost && ghost[i]) { lbl = 0; tmp = ghost[i] == 2 ? TMP_GHOST_B : TMP_GHOST; }   // slab engine
+      else if (b) { lbl = 0; tmp = TMP_B; }
+      else if (a) { lbl = 0; tmp = (stamp_of(0) << 16) | (unsigned)lblA; }
+      s.sw[i] = ((unsigned long long)tmp << 32) | lbl;
+    }
     if (s.res) {
       if (d <= 2) reinterpret_cast<uint32_t*>(s.res)[i] = 0u;
       else reinterpret_cast<unsigned long long*>(s.res)[i] = 0ull;

@@ -240,9 +240,21 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
   __syncthreads();
   const unsigned n = min(sm.np, (unsigned)QP_CAP);
   const unsigned ns = min(sm.nspill, s.spill_cap);
+  unsigned appended = 0;
   for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
     const unsigned o = sm.ofill[d];
-    if (o) { sm.rfill[d] += min(o, sm.rcap[d] - sm.rfill[d]); sm.ofill[d] = 0; }
+    if (o) {
+      const unsigned a = min(o, sm.rcap[d] - sm.rfill[d]);
+      sm.rfill[d] += a;
+      sm.ofill[d] = 0;
+      appended += a;
+    }
+  }
+  // staging-overflow statistics (rare paths; tests check they were exercised)
+  if (appended) atomicAdd(&s.ctl->n_appended, (unsigned long long)appended);
+  if (threadIdx.x == 0 && sm.nspill) {
+    atomicAdd(&s.ctl->n_spilled, (unsigned long long)ns);
+    if (sm.nspill > ns) atomicAdd(&s.ctl->n_single, (unsigned long long)(sm.nspill - ns));
   }
   if (n > 0) flush_sorted(s, sm, t, region, n);
   const unsigned long long* sp = s.spill + (size_t)(blockIdx.x - s.blk0) * s.spill_cap;
@@ -291,7 +303,10 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   const unsigned nd = min(__ldcg(s.bndesc + slot), s.dcap);
   const unsigned long long* dl = s.bdesc + slot * s.dcap;
   constexpr unsigned CH = FI * 32;
-  constexpr unsigned MAXD = 512;
+  // run descriptors staged per pass: dpos[MAXD] (u64) + dchunk[MAXD + 1] (u32) in the wl union
+  constexpr unsigned WL_BYTES = sizeof(Smem::wl);
+  constexpr unsigned MAXD = ((WL_BYTES - 4) / 12 >= 512 ? 512u : ((WL_BYTES - 4) / 12) & ~31u);
+  static_assert(MAXD >= 32 && MAXD * 8 + (MAXD + 1) * 4 <= WL_BYTES, "descriptor staging exceeds Smem::wl");
   unsigned long long* dpos = reinterpret_cast<unsigned long long*>(&sm.wl[0][0]);   // [MAXD]
   unsigned* dchunk = reinterpret_cast<unsigned*>(dpos + MAXD);                        // [MAXD + 1] prefix
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
@@ -887,6 +902,7 @@ __device__ __forceinline__ bool peer_sync(const Dev& s, Smem& sm, unsigned long 
         if (propose) {
           long long need = 0;
           s.ctl->prop = wheel_propose(s, *propose, &need);
+          s.ctl->prop_need = need;     // read back by this same thread in the decision
         }
         __threadfence_system();
         red_add_release_sys(s.xbar, 1ull);
@@ -951,7 +967,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_peer(const __grid_const
         G.pending = max(G.pending, (long long)p->pending); G.overflow = max(G.overflow, (long long)p->overflow);
       }
       View nv = v;
-      wheel_decide(s, nv, leader, &G);
+      // the slab's own proposal was computed by its leader in peer_sync (only the writer needs its
+      // ring need); the decision itself uses the combined G, so nobody re-runs wheel_propose here
+      wheel_decide(s, nv, leader, &G, &G, leader ? s.ctl->prop_need : 0);
       sm.view = nv;
     }
     __syncthreads();

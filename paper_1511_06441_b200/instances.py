@@ -138,8 +138,10 @@ def grid_values(shape, seed: int, lo: int, hi: int, chunk: int = 1 << 22):
 def set_mask(shape, rule) -> np.ndarray:
     """A/B vertex sets.  rule: 'face0' (x0 = 0), 'face1' (x0 = n0-1), 'corner0'
     (v = 0), 'corner1' (v = N-1), 'centre' (floor(n/2) per axis),
-    'boundary' (any x_k in {0, n_k-1}, the §6 protocol), or an
-    explicit iterable of vertex indices."""
+    'boundary' (any x_k in {0, n_k-1}, the §6 protocol),
+    'checker' (even coordinate sum: every neighbour of a member is a non-member,
+    so the initial treatment starts an edge on every lane — a dense-treat stress
+    case), or an explicit iterable of vertex indices."""
     N = int(np.prod(shape, dtype=np.int64))
     m = np.zeros(N, dtype=np.uint8)
     if isinstance(rule, str):
@@ -153,6 +155,12 @@ def set_mask(shape, rule) -> np.ndarray:
                 v += (n // 2) * mul
                 mul *= n
             m[v] = 1
+        elif rule == "checker":
+            v = np.arange(N, dtype=np.int64)
+            par = np.zeros(N, dtype=np.int64)
+            for k in range(len(shape)):
+                par += axis_coord(shape, k, v)
+            m[par % 2 == 0] = 1
         elif rule in ("face0", "face1", "boundary"):
             v = np.arange(N, dtype=np.int64)
             x0 = axis_coord(shape, 0, v)

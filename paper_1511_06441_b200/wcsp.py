@@ -20,7 +20,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("WCSP_LIB") or os.path.join(_PKG, "libwcsp.so")   # WCSP_LIB: A/B builds
 
 M_INF = -1
-M_MAX = 65533
+M_MAX = 65533            # 16-bit label layout (the fast default)
+M_MAX_WIDE = 2147483646  # larger budgets run on 32-bit labels (include/wcsp.h)
 REACHED, INFEASIBLE, EINVAL, EMISMATCH, EBUDGET, ENOMEM, ECUDA, ENCCL, EOVERFLOW = range(9)
 MEM_HOST, MEM_DEVICE = 0, 1
 JUMP, UNIT = 0, 1
@@ -61,7 +62,8 @@ class _Result(ctypes.Structure):
                 ("relabels", ctypes.c_int64), ("lanes_started", ctypes.c_int64), ("peak_active", ctypes.c_int64),
                 ("peak_phantoms", ctypes.c_int64), ("phantom_capacity", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("device_ms", ctypes.c_double),
-                ("cycle_ms", ctypes.c_double)]
+                ("cycle_ms", ctypes.c_double), ("retries", ctypes.c_int64), ("staging_appended", ctypes.c_int64),
+                ("staging_spilled", ctypes.c_int64), ("staging_singles", ctypes.c_int64)]
 
 
 TRACE_FIELDS = ["t", "delta", "active_vertices", "live_lanes", "phantoms", "triggered", "arrivals",
@@ -142,6 +144,10 @@ class Result:
     kernel_launches: int = 0
     device_ms: float = 0.0
     cycle_ms: float = 0.0
+    retries: int = 0
+    staging_appended: int = 0
+    staging_spilled: int = 0
+    staging_singles: int = 0
 
     def key(self):
         """Outputs compared bit-exactly with the oracle: (status, F1, F2, X, Y)."""

@@ -1,4 +1,4 @@
-"""Write paper_1511_06441_b200/data/mbind.json: the binding budget of each
+"""Write tests/golden/mbind.json: the binding budget of each
 bench/test workload, M_bind = floor((F2_min + F2_lex)/2) + 1 (SURVEY §8
 notation), from the CPU oracle's tier-3 Dijkstras ONLY (oracle/), never from
 the CUDA path.  F2_min = min weight of an A->B path; F2_lex = weight of the
@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 from paper_1511_06441_b200 import instances as I  # noqa: E402
 
-OUT = os.path.join(ROOT, "paper_1511_06441_b200", "data", "mbind.json")
+OUT = os.path.join(ROOT, "tests", "golden", "mbind.json")
 SHAPES = {"C2": (1024, 1024), "C3": (256, 256, 256), "C3s": (128, 128, 128), "C5": (1024, 1024, 1024),
           # §6 protocol: water on the cube's boundary, B = the centre vertex
           "P6-50": (50, 50, 50), "P6-75": (75, 75, 75), "P6-100": (100, 100, 100), "P6-125": (125, 125, 125)}

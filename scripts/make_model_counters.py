@@ -18,14 +18,14 @@ from paper_1511_06441_b200 import instances as I  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "tests", "golden", "model_counters.json")
-MBIND = json.load(open(os.path.join(ROOT, "paper_1511_06441_b200", "data", "mbind.json")))
+MBIND = json.load(open(os.path.join(ROOT, "tests", "golden", "mbind.json")))
 SHAPES = {"C2": (1024, 1024), "C3": (256, 256, 256), "C3s": (128, 128, 128)}
 
 
 def main(keys):
     out = json.load(open(OUT)) if os.path.exists(OUT) else {
         "_source": "scripts/make_model_counters.py: oracle.solve_model (tier 5, jump time) on "
-                   "instances.config_face(shape, seed) at M = M_bind (data/mbind.json)"}
+                   "instances.config_face(shape, seed) at M = M_bind (tests/golden/mbind.json)"}
     for key in keys:
         name, seed = key.split("/")
         inst = I.config_face(SHAPES[name], int(seed), I.M_INF).with_M(MBIND[key]["M_bind"])

@@ -69,3 +69,19 @@ def test_compute_entry_points_fail_loudly_without_gpu():
     with pytest.raises(wcsp.WcspError) as e:
         wcsp.solve(I.fixture_B())
     assert e.value.status == wcsp.ECUDA
+
+
+def test_budget_range_is_validated_before_any_device_work():
+    """M beyond the wide-label range (include/wcsp.h WCSP_M_MAX_WIDE) or M < 1 is
+    WCSP_EINVAL; a budget above the 16-bit range is NOT an error (PAPER.md:20,
+    M in R+) — without a GPU it gets as far as the device (WCSP_ECUDA)."""
+    import torch
+    for bad in (0, -5, wcsp.M_MAX_WIDE + 1, 1 << 40):
+        with pytest.raises(wcsp.WcspError) as e:
+            wcsp.solve(I.fixture_B().with_M(bad))
+        assert e.value.status == wcsp.EINVAL, bad
+    if not torch.cuda.is_available():
+        for ok in (wcsp.M_MAX + 1, 10 ** 6, wcsp.M_MAX_WIDE):
+            with pytest.raises(wcsp.WcspError) as e:
+                wcsp.solve(I.fixture_B().with_M(ok))
+            assert e.value.status == wcsp.ECUDA, ok

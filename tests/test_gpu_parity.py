@@ -512,9 +512,9 @@ def test_stamp_wrap_long_run(engine):
 @pytest.mark.skipif(os.environ.get("WCSP_TEST_C5") != "1", reason="C5 (1024^3, ~105 GB of HBM, ~6 min): set WCSP_TEST_C5=1")
 def test_C5_full_size_one_gpu():
     """configs[4] unsliced on one B200: at both M endpoints the oracle's tier-3
-    values (scripts/make_mbind.py, data/mbind.json) are reproduced exactly;
+    values (scripts/make_mbind.py, tests/golden/mbind.json) are reproduced exactly;
     at M_bind the run satisfies F2 < M and F1_lex <= F1 <= F1 at F2_min (P5)."""
-    table = json.load(open(os.path.join(os.path.dirname(I.__file__), "data", "mbind.json")))
+    table = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "mbind.json")))
     g = table["C5/0"]
     inst = I.config_face((1024, 1024, 1024), 0, g["M_bind"])
     with wcsp.Solver(inst, engine="wheel") as s:

@@ -894,8 +894,8 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
       const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
       const bool test = trig && f1j != 0 && lstar - (int)f2j > 0;
-      rl[j] = test ? (int)__ldcg(s.lab + q + s.off[j]) : (int)LBL_REMOVED_W;
-      rtw[j] = test ? __ldcg(s.sw + q + s.off[j]) : 0ull;
+      rl[j] = test ? (int)__ldcg(s.lab + (q + s.off[j])) : (int)LBL_REMOVED_W;
+      rtw[j] = test ? __ldcg(s.sw + (q + s.off[j])) : 0ull;
     }
     LW neww = 0;
 #pragma unroll

@@ -44,6 +44,8 @@ WORKLOADS = {
     "C5": {"shape": (1024, 1024, 1024), "desc": "configs[4]: 3D 1024^3 cube, f1,f2 ~ U{1..10}, face x=0 -> face "
                                                 "x=1023, M = M_bind; unsliced on one B200 (about 105 GB of HBM) or "
                                                 "z-slabs over N GPUs with --partition slabs"},
+    "C5z8": {"shape": (1024, 1024, 128), "desc": "one z-slab of configs[4] at 8 GPUs: 1024x1024x128, f1,f2 ~ "
+                                                 "U{1..10}, face x=0 -> face x=1023, M = M_bind (DRAM-resident state)"},
     "C4": {"shape": None, "desc": "configs[3]: Theorem-2 fractal omega_k, k = 10 (t = 1024), V = [-t,t]x[0,t+1], "
                                   "A = x-axis, B = (0,t), f1 in {1,2}, f2 = 1, M = infinity"},
 }
@@ -344,10 +346,42 @@ def run_ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1511_06441_b200 import wcsp
 
-    inst, meta = workload_instance(args.workload, 0 if slabs else rank)
-    d = len(inst.shape)
     stream = torch.cuda.current_stream()
-    if slabs:   # one instance, slab `rank` of `world` on this GPU
+    shape = WORKLOADS[args.workload]["shape"]
+    on_device = (shape is not None and int(np.prod(shape)) >= (1 << 27) and not slabs and args.vslabs <= 1
+                 and not args.cpu_full)
+    face = args.workload in ("C2", "C3", "C3s", "C5", "C5z8")
+    if slabs and face:
+        # slab partition: every rank generates ONLY its planes (slab + ghost planes) in HBM and
+        # passes them with local_slab (no rank ever holds the whole grid; include/wcsp.h)
+        meta = json.load(open(MBIND))[f"{args.workload}/0"]
+        z0, z1, p0, p1 = wcsp.slab_planes(shape[-1], world, rank)
+        f1, f2 = wcsp.generate_grid(shape, meta["seed"], 1, 10, p0, p1, stream=stream)
+        A = wcsp.generate_mask(shape, "face0", p0, p1, stream=stream)
+        B = wcsp.generate_mask(shape, "face1", p0, p1, stream=stream)
+        torch.cuda.synchronize()
+        from types import SimpleNamespace
+        inst = SimpleNamespace(shape=tuple(shape), M=meta["M_bind"], name=args.workload)
+        solver = wcsp.Solver(shape=shape, f1=f1, f2=f2, maskA=A, maskB=B, M=inst.M, engine="wheel", stream=stream,
+                             nranks=world, rank=rank, nccl_id=share_nccl_id(rank), halo=args.halo, local_slab=True)
+        del f1, f2, A, B
+    elif on_device:
+        # 2^27+ vertices: generate the instance in HBM (wcsp_generate_grid, the same recipe as
+        # instances.grid_values) instead of building GBs of host arrays
+        meta = json.load(open(MBIND))[f"{args.workload}/0"]
+        f1, f2 = wcsp.generate_grid(shape, meta["seed"], 1, 10, stream=stream)
+        A, B = wcsp.generate_mask(shape, "face0", stream=stream), wcsp.generate_mask(shape, "face1", stream=stream)
+        from types import SimpleNamespace
+        inst = SimpleNamespace(shape=tuple(shape), M=meta["M_bind"], name=args.workload)
+        solver = wcsp.Solver(shape=shape, f1=f1, f2=f2, maskA=A, maskB=B, M=inst.M, engine=args.engine,
+                             stream=stream)
+        args.e2e_steps = 0
+    else:
+        inst, meta = workload_instance(args.workload, 0 if slabs else rank)
+    d = len(inst.shape)
+    if on_device or (slabs and face):
+        pass
+    elif slabs:   # one instance, slab `rank` of `world` on this GPU
         solver = wcsp.Solver(inst, engine="wheel", stream=stream, nranks=world, rank=rank,
                              nccl_id=share_nccl_id(rank), halo=args.halo)
     elif args.vslabs > 1:

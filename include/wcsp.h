@@ -128,6 +128,14 @@ typedef struct {
   int32_t rank;
   const uint8_t* nccl_id;   /* 128 bytes from wcsp_nccl_unique_id() on one rank, shared with all;
                                non-NULL with nranks = 1 runs the NCCL path on one GPU */
+  int32_t local_slab;       /* multi-GPU only (nccl_id set): 1 = the problem's arrays hold ONLY this
+                               rank's planes [p0, p1) of the last axis (wcsp_slab_planes: its slab
+                               plus one ghost plane per neighbour), laid out as the whole-grid arrays
+                               with N replaced by (p1 - p0) * plane; problem.shape stays the global
+                               shape; host or device memory.  Each rank validates its own planes and
+                               the counts are combined over NCCL, so no rank ever holds (or scans)
+                               the whole grid — a 1024^3 cube over 8 GPUs.  0 = every
+                               rank passes the whole problem (host arrays). */
 } wcsp_options;
 
 typedef struct {
@@ -213,6 +221,31 @@ wcsp_status wcsp_validate_path(const wcsp_problem* problem, const int64_t* path,
  * else WCSP_INFEASIBLE; result = the last step's solve record. */
 wcsp_status wcsp_staircase(wcsp_handle* h, int64_t M_max, int64_t f2_stop, int64_t* steps, int64_t cap,
                            int64_t* n, wcsp_result* result);
+/* Seeded synthetic instances generated in device memory (DESIGN.md §4 recipe; the same pure
+ * function as the host generator paper_1511_06441_b200/instances.py, so a rank can build only
+ * its own slab of a large cube in HBM).  Not part of the method: input preparation only.
+ * wcsp_generate_grid: f1, f2 of the planes [z0, z1) of the LAST axis of `shape` (z1 < 0: to the
+ * end), written as f1[k * Nl + i] (Nl = (z1 - z0) * plane, i = global index - z0 * plane):
+ * value = lo + ((h >> 32) mod (hi - lo + 1)), h = sm(sm(seed) ^ (8v + 2k + c)), c = 0 for f1 and
+ * 1 for f2, sm = the splitmix64 finaliser of x + 0x9E3779B97F4A7C15; 0 where x_k = n_k - 1.
+ * 1 <= lo <= hi <= 255.  f1, f2: device buffers of d * Nl bytes, written on `stream` (asynchronous).
+ * wcsp_generate_mask: out[i] = 1 if the vertex belongs to the set `rule` (below), else 0.
+ * Errors: WCSP_EINVAL for a bad shape / range / rule / NULL pointer, WCSP_ECUDA on a launch error. */
+enum { WCSP_SET_FACE0 = 0,        /* x0 = 0 (A of the face-to-face configs) */
+       WCSP_SET_FACE1 = 1,        /* x0 = n0 - 1 (their B) */
+       WCSP_SET_BOUNDARY = 2,     /* any x_k in {0, n_k - 1}: water on the boundary */
+       WCSP_SET_CENTRE = 3,       /* floor(n_k / 2) on every axis (reading R18) */
+       WCSP_SET_CORNER0 = 4,      /* v = 0 */
+       WCSP_SET_CORNER1 = 5 };    /* v = N - 1 */
+wcsp_status wcsp_generate_grid(int32_t d, const int64_t* shape, uint64_t seed, int32_t lo, int32_t hi, int64_t z0,
+                               int64_t z1, uint8_t* f1, uint8_t* f2, void* stream);
+wcsp_status wcsp_generate_mask(int32_t d, const int64_t* shape, int32_t rule, int64_t z0, int64_t z1, uint8_t* out,
+                               void* stream);
+/* The planes of the last axis a rank holds in the slab partition: slab `rank` of
+ * `nranks` owns z in [out[0], out[1]) = [rank * n_last / nranks, (rank + 1) * n_last / nranks) and
+ * its local arrays (options.local_slab) cover [out[2], out[3]) = the slab plus one ghost plane on
+ * each side that has a neighbour.  Host-only arithmetic; WCSP_EINVAL for a bad argument. */
+wcsp_status wcsp_slab_planes(int64_t n_last, int32_t nranks, int32_t rank, int64_t* out4);
 /* NCCL unique id (128 bytes) for options.nccl_id; call on one rank and share it
  * (e.g. through torch.distributed).  Returns WCSP_ENCCL if NCCL cannot be loaded. */
 wcsp_status wcsp_nccl_unique_id(uint8_t* out128);

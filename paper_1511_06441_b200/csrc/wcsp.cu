@@ -3,6 +3,7 @@
 #include "wcsp.h"
 #include "wcsp_device.cuh"
 #include "wcsp_wheel.cuh"
+#include "wcsp_gen.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -83,6 +84,7 @@ struct wcsp_handle {
   unsigned long long* d_cnt = nullptr;               // validation counters
   long long M = 0;
   int nsm = 0, grid = 0;
+  long long l2_bytes = 0;
   int grid_main = 0;                                 // grid of opt.engine's cycle kernel (grid = this solve's)
   bool big = false;                                  // wheel: the 4-blocks-per-SM cycle kernel
   // wide labels (M > WCSP_M_MAX): this solve runs the sweep engine on u32 labels + u64 temps
@@ -168,11 +170,22 @@ cudaError_t set_smem_attrs() {
 // so a round count just above an integer leaves most warps idle in the last round: take 16
 // words when that gives at most one round or at least four (C2, C3), else 8 (C3s, P6 cubes).
 // WCSP_WIN_WORDS overrides (A/B runs).
+// Interleaved treat rounds (phase_treat): on grids whose vertex state words are several times the
+// L2, every block's round r lies in one chunk of the grid so that the whole device works on one
+// L2-sized chunk of the front at a time (the fire then follows the same order).  WCSP_ILEAVE=0/1
+// overrides (A/B runs).
+bool ileave_for(const wcsp_handle* h);
+
 unsigned win_words_for(unsigned nwords, unsigned nblocks) {
   if (const char* e = getenv("WCSP_WIN_WORDS")) return atoi(e) >= WIN_WORDS ? (unsigned)WIN_WORDS : atoi(e) >= 16 ? 16u : 8u;
   if (nblocks == 0) return 8u;
   const double rounds16 = (double)nwords / (16.0 * nblocks * WARPS);
   return std::min<unsigned>(rounds16 <= 1.0 || rounds16 >= 4.0 ? 16u : 8u, (unsigned)WIN_WORDS);
+}
+
+bool ileave_for(const wcsp_handle* h) {
+  if (const char* e = getenv("WCSP_ILEAVE")) return atoi(e) != 0;
+  return (unsigned long long)h->N * sizeof(unsigned long long) > 2ull * (unsigned long long)h->l2_bytes;
 }
 
 Dev make_dev(const wcsp_handle* h) {
@@ -225,6 +238,7 @@ Dev make_dev(const wcsp_handle* h) {
                                        : (unsigned long long)h->grid * 64ull;
   s.nblocks = (unsigned)h->grid;
   s.win_words = win_words_for(s.nwords, s.nblocks);
+  s.ileave = ileave_for(h);
   s.goff = h->goff;
   s.plane = h->plane;
   s.ghost_hi_start = h->ghi ? h->ghost_hi_start : (unsigned)h->N;
@@ -682,6 +696,11 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
     h->own_stream = true;
   }
   CKC(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->dev));
+  {
+    int l2 = 0;
+    CKC(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->dev));
+    h->l2_bytes = l2;
+  }
   switch (p->d) {
     case 1: CKC(set_smem_attrs<1>()); break;
     case 2: CKC(set_smem_attrs<2>()); break;
@@ -845,8 +864,34 @@ wcsp_status host_validate(const wcsp_problem* p, unsigned long long* nB, int* f1
 void* peer_fn_d(int d, bool big);
 wcsp_status peer_connect(wcsp_handle* g);
 
+// options.local_slab: counts of the validation rules (include/wcsp.h) over the planes [z0, z1) a
+// rank owns, from its local arrays that start at plane p0 ([0] |A|, [1] |B|, [2] |A n B|, [3]
+// present edges with f2 = 0, [4] max f1); every edge (v, v + e_k) is stored at v, so summing the
+// owners' counts checks each vertex and edge of the grid exactly once.
+void local_counts(const wcsp_problem* p, long long Nl, long long plane, long long p0, long long z0, long long z1,
+                  unsigned long long c[5]) {
+  long long st[4] = {1, 1, 1, 1}, N = 1;
+  for (int k = 0; k < p->d; ++k) { st[k] = N; N *= p->shape[k]; }
+  for (int i = 0; i < 5; ++i) c[i] = 0;
+  for (long long vl = (z0 - p0) * plane; vl < (z1 - p0) * plane; ++vl) {
+    const long long v = p0 * plane + vl;
+    const bool pr = p->present == nullptr || p->present[vl] != 0;
+    const bool a = pr && p->maskA[vl], b = pr && p->maskB[vl];
+    c[0] += a; c[1] += b; c[2] += a && b;
+    for (int k = 0; k < p->d; ++k) {
+      if ((v / st[k]) % p->shape[k] + 1 < p->shape[k]) {
+        const uint8_t f1 = p->f1[(size_t)k * Nl + vl], f2 = p->f2[(size_t)k * Nl + vl];
+        c[3] += f1 != 0 && f2 == 0;
+        c[4] = std::max<unsigned long long>(c[4], f1);
+      }
+    }
+  }
+}
+
 wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_handle** out) {
-  if (p->mem != WCSP_MEM_HOST) return fail(WCSP_EINVAL, "the slab engine takes host arrays");
+  const bool local = opt.local_slab != 0;
+  if (local && !opt.nccl_id) return fail(WCSP_EINVAL, "local_slab needs the multi-GPU slab engine (nccl_id)");
+  if (p->mem != WCSP_MEM_HOST && !local) return fail(WCSP_EINVAL, "the slab engine takes host arrays");
   if (!is_wheel(opt.engine)) return fail(WCSP_EINVAL, "the slab engine runs the wheel engine (engine = WHEEL)");
   if (wide_M(p->M)) return fail(WCSP_EINVAL, "slab engine: M > %d (wide labels) is single-device only", WCSP_M_MAX);
   const bool dist = opt.nccl_id != nullptr && opt.nranks >= 1;   // nranks = 1: NCCL path on one GPU (tests)
@@ -865,8 +910,8 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
   const bool peer_big = opt.halo == WCSP_HALO_PEER && (bps ? atoi(bps) >= 4 : d >= 3 && N >= (1ll << 21));
   unsigned long long nB = 0;
   int f1max = 1;
-  wcsp_status st = host_validate(p, &nB, &f1max);
-  if (st != WCSP_REACHED) return st;
+  wcsp_status st = WCSP_REACHED;
+  if (!local && (st = host_validate(p, &nB, &f1max)) != WCSP_REACHED) return st;
   wcsp_handle* g = new wcsp_handle();
   g->opt = opt;
   g->d = d;
@@ -889,6 +934,63 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
     return bail(fail(WCSP_ECUDA, "event creation failed"));
   g->rank = dist ? opt.rank : 0;
   g->nranks = dist ? opt.nranks : 1;
+  if (dist) {                      // the communicator first: local slabs combine their validation over it
+    ncclUniqueId id;
+    memcpy(&id, opt.nccl_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    const ncclResult_t nr = nccl_api().commInitRank(&comm, opt.nranks, id, opt.rank);
+    if (nr != ncclSuccess) return bail(fail(WCSP_ENCCL, "ncclCommInitRank: %s", nccl_api().errStr(nr)));
+    g->comm = comm;
+  }
+  // local_slab: this rank's arrays cover planes [lp0, lp1) only (device arrays are brought to the
+  // host once, slab-sized); validate the owned planes and combine the counts over NCCL
+  wcsp_problem lpb = *p;
+  std::vector<uint8_t> hf1, hf2, hA, hB, hP;
+  long long lp0 = 0;
+  if (local) {
+    long long zz[4];
+    if ((st = wcsp_slab_planes(nL, R, opt.rank, (int64_t*)zz)) != WCSP_REACHED) return bail(st);
+    lp0 = zz[2];
+    const long long Nl = (zz[3] - zz[2]) * plane;
+    if (p->mem == WCSP_MEM_DEVICE) {
+      hf1.resize((size_t)d * Nl); hf2.resize((size_t)d * Nl); hA.resize(Nl); hB.resize(Nl);
+      if (cudaMemcpy(hf1.data(), p->f1, hf1.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(hf2.data(), p->f2, hf2.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(hA.data(), p->maskA, Nl, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(hB.data(), p->maskB, Nl, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return bail(fail(WCSP_ECUDA, "local slab: reading the device arrays failed"));
+      if (p->present) {
+        hP.resize(Nl);
+        if (cudaMemcpy(hP.data(), p->present, Nl, cudaMemcpyDeviceToHost) != cudaSuccess)
+          return bail(fail(WCSP_ECUDA, "local slab: reading present failed"));
+      }
+      lpb.f1 = hf1.data(); lpb.f2 = hf2.data(); lpb.maskA = hA.data(); lpb.maskB = hB.data();
+      lpb.present = p->present ? hP.data() : nullptr;
+      lpb.mem = WCSP_MEM_HOST;
+    }
+    unsigned long long c[5];
+    local_counts(&lpb, Nl, plane, zz[2], zz[0], zz[1], c);
+    NcclApi& nc = nccl_api();
+    unsigned long long* dc = nullptr;
+    unsigned long long h4[4] = {c[0], c[1], c[2], c[3]}, hm = c[4];
+    if (cudaMalloc(&dc, 5 * sizeof(unsigned long long)) != cudaSuccess) return bail(fail(WCSP_ENOMEM, "counts"));
+    cudaMemcpy(dc, h4, sizeof(h4), cudaMemcpyHostToDevice);
+    cudaMemcpy(dc + 4, &hm, sizeof(hm), cudaMemcpyHostToDevice);
+    ncclResult_t r1 = nc.allReduce(dc, dc, 4, ncclUint64, ncclSum, (ncclComm_t)g->comm, g->stream);
+    ncclResult_t r2 = nc.allReduce(dc + 4, dc + 4, 1, ncclUint64, ncclMax, (ncclComm_t)g->comm, g->stream);
+    cudaStreamSynchronize(g->stream);
+    cudaMemcpy(h4, dc, sizeof(h4), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&hm, dc + 4, sizeof(hm), cudaMemcpyDeviceToHost);
+    cudaFree(dc);
+    if (r1 != ncclSuccess || r2 != ncclSuccess) return bail(fail(WCSP_ENCCL, "validation allreduce failed"));
+    if (h4[0] == 0) return bail(fail(WCSP_EINVAL, "A is empty (among present vertices)"));
+    if (h4[1] == 0) return bail(fail(WCSP_EINVAL, "B is empty (among present vertices)"));
+    if (h4[2]) return bail(fail(WCSP_EINVAL, "A and B intersect in %llu vertices", h4[2]));
+    if (h4[3]) return bail(fail(WCSP_EINVAL, "%llu present edges have f1 > 0 and f2 = 0", h4[3]));
+    nB = h4[1];
+    f1max = std::max<int>(1, (int)hm);
+  }
+  const wcsp_problem* src = local ? &lpb : p;
   for (int i = 0; i < R; ++i) {
     if (dist && i != opt.rank) continue;          // one slab per process
     SlabSpec sp{};
@@ -903,17 +1005,21 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
     sp.nB = nB;
     sp.f1max = f1max;
     sp.per_sm = peer_big ? 4 : 0;
+    // the slab's planes in the source arrays: the whole grid's (offset lo) or the local ones (offset
+    // lo - lp0 * plane within arrays of SN vertices)
+    const long long SN = local ? (long long)(((lo / plane) - lp0) * plane + Nl) : N;
+    const long long so = local ? lo - lp0 * plane : lo;
     std::vector<uint8_t> f1((size_t)d * Nl), f2((size_t)d * Nl), A(Nl), B(Nl), ghost(Nl, 0), pres;
     for (int k = 0; k < d; ++k) {
-      memcpy(&f1[(size_t)k * Nl], p->f1 + (size_t)k * N + lo, Nl);
-      memcpy(&f2[(size_t)k * Nl], p->f2 + (size_t)k * N + lo, Nl);
+      memcpy(&f1[(size_t)k * Nl], src->f1 + (size_t)k * SN + so, Nl);
+      memcpy(&f2[(size_t)k * Nl], src->f2 + (size_t)k * SN + so, Nl);
     }
-    memcpy(A.data(), p->maskA + lo, Nl);
-    memcpy(B.data(), p->maskB + lo, Nl);
-    if (p->present) { pres.resize(Nl); memcpy(pres.data(), p->present + lo, Nl); }
+    memcpy(A.data(), src->maskA + so, Nl);
+    memcpy(B.data(), src->maskB + so, Nl);
+    if (src->present) { pres.resize(Nl); memcpy(pres.data(), src->present + so, Nl); }
     auto mark_ghost = [&](long long first) {
       for (long long j = first; j < first + plane; ++j) {
-        const bool pr = p->present == nullptr || pres[j] != 0;
+        const bool pr = src->present == nullptr || pres[j] != 0;
         ghost[j] = pr ? (B[j] ? 2 : 1) : 0;
         A[j] = 0;
         B[j] = 0;
@@ -925,7 +1031,8 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
     wcsp_problem lp = *p;
     lp.shape[d - 1] = sp.z1 - sp.z0 + sp.glo + sp.ghi;
     lp.f1 = f1.data(); lp.f2 = f2.data(); lp.maskA = A.data(); lp.maskB = B.data();
-    lp.present = p->present ? pres.data() : nullptr;
+    lp.present = src->present ? pres.data() : nullptr;
+    lp.mem = WCSP_MEM_HOST;
     wcsp_options co = opt;
     co.slabs = 0;
     co.engine = WCSP_ENGINE_WHEEL_STEPPED;
@@ -933,14 +1040,6 @@ wcsp_status create_group(const wcsp_problem* p, const wcsp_options& opt, wcsp_ha
     wcsp_handle* ch = nullptr;
     if ((st = create_impl(&lp, co, &sp, &ch)) != WCSP_REACHED) return bail(st);
     g->children.push_back(ch);
-  }
-  if (dist) {
-    ncclUniqueId id;
-    memcpy(&id, opt.nccl_id, sizeof(id));
-    ncclComm_t comm = nullptr;
-    const ncclResult_t nr = nccl_api().commInitRank(&comm, opt.nranks, id, opt.rank);
-    if (nr != ncclSuccess) return bail(fail(WCSP_ENCCL, "ncclCommInitRank: %s", nccl_api().errStr(nr)));
-    g->comm = comm;
   }
   std::vector<Ctl*> ctls;
   for (auto* ch : g->children) ctls.push_back(ch->ctl);
@@ -1269,6 +1368,7 @@ Dev make_peer_dev(wcsp_handle* g, int i) {
   s.slab = 1;
   s.nblocks = g->peer_per;
   s.win_words = win_words_for(s.nwords, s.nblocks);
+  s.ileave = ileave_for(c);
   s.blk0 = dist ? 0u : (unsigned)i * g->peer_per;
   s.plo_end = c->glo ? c->plane : 0u;
   if (dist) {
@@ -1672,6 +1772,64 @@ wcsp_status wcsp_staircase(wcsp_handle* h, int64_t M_max, int64_t f2_stop, int64
   }
   if (result) *result = r;
   return st;
+}
+
+wcsp_status wcsp_slab_planes(int64_t n_last, int32_t nranks, int32_t rank, int64_t* out4) {
+  if (!out4 || nranks < 1 || rank < 0 || rank >= nranks || n_last < nranks)
+    return fail(WCSP_EINVAL, "slab planes: need 0 <= rank < nranks <= n_last (got %d, %d, %lld)", rank, nranks,
+                (long long)n_last);
+  out4[0] = (int64_t)rank * n_last / nranks;
+  out4[1] = (int64_t)(rank + 1) * n_last / nranks;
+  out4[2] = out4[0] - (rank > 0 ? 1 : 0);
+  out4[3] = out4[1] + (rank < nranks - 1 ? 1 : 0);
+  return WCSP_REACHED;
+}
+
+static wcsp_status gen_shape(int32_t d, const int64_t* shape, int64_t z0, int64_t z1, GenShape* g) {
+  if (d < 1 || d > 4 || !shape) return fail(WCSP_EINVAL, "d = %d outside 1..4 (or shape NULL)", d);
+  g->d = d;
+  long long N = 1;
+  for (int k = 0; k < 4; ++k) {
+    g->n[k] = k < d ? shape[k] : 1;
+    if (g->n[k] < 1) return fail(WCSP_EINVAL, "shape[%d] < 1", k);
+    N *= g->n[k];
+  }
+  if (N > (1ll << 30)) return fail(WCSP_EINVAL, "N > 2^30 vertices");
+  const long long nL = g->n[d - 1];
+  if (z1 < 0) z1 = nL;
+  if (z0 < 0 || z0 > z1 || z1 > nL) return fail(WCSP_EINVAL, "plane range [%lld, %lld) outside [0, %lld]", z0, z1, nL);
+  g->plane = N / nL;
+  g->v0 = z0 * g->plane;
+  g->Nl = (z1 - z0) * g->plane;
+  return WCSP_REACHED;
+}
+
+wcsp_status wcsp_generate_grid(int32_t d, const int64_t* shape, uint64_t seed, int32_t lo, int32_t hi, int64_t z0,
+                               int64_t z1, uint8_t* f1, uint8_t* f2, void* stream) {
+  GenShape g;
+  wcsp_status st;
+  if ((st = gen_shape(d, shape, z0, z1, &g)) != WCSP_REACHED) return st;
+  if (lo < 1 || hi < lo || hi > 255) return fail(WCSP_EINVAL, "value range [%d, %d] outside 1..255", lo, hi);
+  if (g.Nl == 0) return WCSP_REACHED;           // an empty plane range writes nothing
+  if (!f1 || !f2) return fail(WCSP_EINVAL, "f1 and f2 must be device pointers");
+  const int blocks = (int)std::min<long long>((g.Nl + 255) / 256, 148ll * 16);
+  k_gen_grid<<<blocks, 256, 0, (cudaStream_t)stream>>>(g, splitmix64(seed), (unsigned)lo, (unsigned)(hi - lo + 1), f1, f2);
+  CK(cudaGetLastError());
+  return WCSP_REACHED;
+}
+
+wcsp_status wcsp_generate_mask(int32_t d, const int64_t* shape, int32_t rule, int64_t z0, int64_t z1, uint8_t* out,
+                               void* stream) {
+  GenShape g;
+  wcsp_status st;
+  if ((st = gen_shape(d, shape, z0, z1, &g)) != WCSP_REACHED) return st;
+  if (rule < WCSP_SET_FACE0 || rule > WCSP_SET_CORNER1) return fail(WCSP_EINVAL, "bad set rule %d", rule);
+  if (g.Nl == 0) return WCSP_REACHED;
+  if (!out) return fail(WCSP_EINVAL, "out must be a device pointer");
+  const int blocks = (int)std::min<long long>((g.Nl + 255) / 256, 148ll * 16);
+  k_gen_mask<<<blocks, 256, 0, (cudaStream_t)stream>>>(g, rule, out);
+  CK(cudaGetLastError());
+  return WCSP_REACHED;
 }
 
 wcsp_status wcsp_nccl_unique_id(uint8_t* out128) {

@@ -153,6 +153,7 @@ struct Dev {
   unsigned* tbits;                 // triggered bitmap (first arrivals of the cycle)
   unsigned nwords;                 // words of the bitmap
   unsigned win_words;              // bitmap words per warp window of the treat (8 or 16)
+  unsigned ileave;                 // treat rounds interleaved across blocks (chunk-at-a-time; see phase_treat)
   unsigned* act[2];
   unsigned long long* pool[2];
   unsigned long long pool_cap;
@@ -1063,7 +1064,12 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   // every block owns one contiguous slab of windows: its phantoms / events come from a
   // compact region of the grid, so a run's destinations share sectors and L2 lines
   const unsigned rounds = (nwin + s.nblocks * WARPS - 1) / (s.nblocks * WARPS);
-  const unsigned win0 = (blockIdx.x - s.blk0) * rounds * WARPS;
+  const unsigned vb = blockIdx.x - s.blk0;
+  const unsigned win0 = vb * rounds * WARPS;
+  // first window of round r: a contiguous slab of windows per block, or (s.ileave, grids whose
+  // state words exceed L2) round r of every block inside one chunk of nblocks * WARPS windows,
+  // so the whole grid treats — and later fires — one L2-sized chunk of the front at a time
+  auto rwin = [&](unsigned r) -> unsigned { return s.ileave ? (r * s.nblocks + vb) * WARPS : win0 + r * WARPS; };
   unsigned dmin = 0xFFFFFFFFu;
   unsigned created = 0, relabels = 0, triggered = 0, lanes_started = 0, tested = 0;   // per thread, this cycle
   if constexpr (WHEEL_ENGINE) {
@@ -1100,13 +1106,13 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
     unsigned short* flat = &sm.wl[0][0];
     const unsigned ww = s.win_words;
 #if WCSP_WIN_PREFETCH
-    unsigned raw = scan && rounds > 0 ? window_load(s, win0 + warp, nwin) : 0u;
+    unsigned raw = scan && rounds > 0 ? window_load(s, rwin(0) + warp, nwin) : 0u;
 #else
-    unsigned bits = scan && rounds > 0 ? window_bits(s, win0 + warp, nwin) : 0u;
+    unsigned bits = scan && rounds > 0 ? window_bits(s, rwin(0) + warp, nwin) : 0u;
 #endif
     for (unsigned r = 0; scan && r < rounds; ++r) {
 #if WCSP_WIN_PREFETCH
-      const unsigned bits = window_use(s, win0 + r * WARPS + warp, raw);
+      const unsigned bits = window_use(s, rwin(r) + warp, raw);
 #endif
       const unsigned cnt = __reduce_add_sync(0xFFFFFFFFu, (unsigned)__popc(bits));
       if (lane == 0) sm.wtot[warp] = cnt;
@@ -1122,11 +1128,11 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
       window_emit(s, bits, base, flat, warp * ww * 32u);
       __syncthreads();
 #if WCSP_WIN_PREFETCH
-      if (r + 1 < rounds) raw = window_load(s, win0 + (r + 1) * WARPS + warp, nwin);   // next round in flight
+      if (r + 1 < rounds) raw = window_load(s, rwin(r + 1) + warp, nwin);   // next round in flight
 #else
-      if (r + 1 < rounds) bits = window_bits(s, win0 + (r + 1) * WARPS + warp, nwin);
+      if (r + 1 < rounds) bits = window_bits(s, rwin(r + 1) + warp, nwin);
 #endif
-      const unsigned rbase = (win0 + r * WARPS) * ww * 32u;
+      const unsigned rbase = rwin(r) * ww * 32u;
       for (unsigned b = warp * 32; b < T; b += WARPS * 32) {
         const unsigned q = b + lane < T ? rbase + flat[b + lane] : 0xFFFFFFFFu;
         treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
@@ -1136,7 +1142,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   }
 #endif
   for (unsigned r = 0; scan && r < rounds; ++r) {
-    const unsigned win = win0 + r * WARPS + warp;
+    const unsigned win = rwin(r) + warp;
     const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
       const unsigned q = b + lane < total ? win * s.win_words * 32u + sm.wl[warp][b + lane] : 0xFFFFFFFFu;

@@ -331,7 +331,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         hi = min(hi, (unsigned long long)s.ghost_hi_start);
       }
       if (hi - lo + 32 > cap) { lo = vlo; hi = vhi; }
-      if (vlo >= vhi || hi <= lo || hi - lo + 32 > cap) { lo = 0; hi = 0; }
+      if (vlo >= vhi || hi <= lo || hi - lo + 32 > cap || s.ileave) { lo = 0; hi = 0; }   // interleaved: no own slab
       lo &= ~31ull;
       sm.bm_lo = (unsigned)lo;
       sm.bm_words = (unsigned)((hi - lo + 31) / 32);
@@ -369,8 +369,13 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
     const unsigned nchunks = dchunk[n];
     // warp w fires a contiguous range of chunks (the descriptor index then advances by at most
     // one per chunk); the first descriptor is found by binary search over the prefix sums
-    const unsigned c_lo = (unsigned)((unsigned long long)nchunks * warp / WARPS);
-    const unsigned c_hi = (unsigned)((unsigned long long)nchunks * (warp + 1) / WARPS);
+    // Interleaved grids (s.ileave): the block's warps take chunks in turn (c = warp, warp + WARPS,
+    // ...), so the whole device walks every run list front to back together and the atomics of a
+    // fire stay inside the L2-sized chunk of the grid the lists were filed from.  Otherwise warp w
+    // fires a contiguous eighth of the list.
+    const unsigned cstep = s.ileave ? (unsigned)WARPS : 1u;
+    const unsigned c_lo = s.ileave ? warp : (unsigned)((unsigned long long)nchunks * warp / WARPS);
+    const unsigned c_hi = s.ileave ? nchunks : (unsigned)((unsigned long long)nchunks * (warp + 1) / WARPS);
     unsigned di = 0;
     {
       unsigned lo = 0, hi = n;                   // largest di with dchunk[di] <= c_lo
@@ -395,10 +400,10 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
     };
     unsigned long long e[FI];
     if (c_lo < c_hi) load_chunk(c_lo, e);
-    for (unsigned c = c_lo; c < c_hi; ++c) {
+    for (unsigned c = c_lo; c < c_hi; c += cstep) {
 #if WCSP_FIRE_PF
       unsigned long long en[FI];   // the next chunk's events load while this one fires
-      if (c + 1 < c_hi) load_chunk(c + 1, en);
+      if (c + cstep < c_hi) load_chunk(c + cstep, en);
 #endif
       unsigned old[FI];
 #pragma unroll
@@ -452,7 +457,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
 #pragma unroll
       for (int it = 0; it < FI; ++it) e[it] = en[it];
 #else
-      if (c + 1 < c_hi) load_chunk(c + 1, e);
+      if (c + cstep < c_hi) load_chunk(c + cstep, e);
 #endif
     }
   }

@@ -51,7 +51,8 @@ class _Options(ctypes.Structure):
                 ("device", ctypes.c_int32), ("cycle_budget", ctypes.c_int64),
                 ("phantom_capacity", ctypes.c_int64), ("trace_cap", ctypes.c_int64),
                 ("stream", ctypes.c_void_p), ("slabs", ctypes.c_int32), ("halo", ctypes.c_int32),
-                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
+                ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("local_slab", ctypes.c_int32)]
 
 
 class _Result(ctypes.Structure):
@@ -76,7 +77,8 @@ class _TraceRec(ctypes.Structure):
 
 EXPORTS = ["wcsp_create", "wcsp_load", "wcsp_solve", "wcsp_set_targets", "wcsp_reconstruct", "wcsp_trace",
            "wcsp_validate_path", "wcsp_destroy", "wcsp_last_error", "wcsp_version", "wcsp_nccl_unique_id",
-           "wcsp_staircase"]
+           "wcsp_staircase", "wcsp_generate_grid", "wcsp_generate_mask", "wcsp_slab_planes"]
+SET_RULES = {"face0": 0, "face1": 1, "boundary": 2, "centre": 3, "corner0": 4, "corner1": 5}
 
 _lib = None
 
@@ -112,6 +114,15 @@ def load_library(path: str = LIB_PATH):
     lib.wcsp_staircase.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
                                    ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), R]
     lib.wcsp_staircase.restype = ctypes.c_int
+    I64P = ctypes.POINTER(ctypes.c_int64)
+    lib.wcsp_generate_grid.argtypes = [ctypes.c_int32, I64P, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    lib.wcsp_generate_grid.restype = ctypes.c_int
+    lib.wcsp_generate_mask.argtypes = [ctypes.c_int32, I64P, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_void_p, ctypes.c_void_p]
+    lib.wcsp_generate_mask.restype = ctypes.c_int
+    lib.wcsp_slab_planes.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]
+    lib.wcsp_slab_planes.restype = ctypes.c_int
     lib.wcsp_nccl_unique_id.argtypes = [ctypes.c_char_p]
     lib.wcsp_nccl_unique_id.restype = ctypes.c_int
     _lib = lib
@@ -201,7 +212,8 @@ class Solver:
     def __init__(self, inst=None, *, shape=None, f1=None, f2=None, maskA=None, maskB=None, present=None,
                  M=None, time_mode: str = "jump", engine: str = "persistent", trace_cap: int = 0,
                  phantom_capacity: int = 0, cycle_budget: int = 0, device: int = 0, stream=None,
-                 slabs: int = 0, halo: str = "copy", nranks: int = 1, rank: int = 0, nccl_id: bytes = None):
+                 slabs: int = 0, halo: str = "copy", nranks: int = 1, rank: int = 0, nccl_id: bytes = None,
+                 local_slab: bool = False):
         lib = load_library()
         self._lib = lib
         self._h = ctypes.c_void_p()
@@ -223,6 +235,7 @@ class Solver:
         o.halo = HALOS[halo]
         o.nranks = int(nranks)
         o.rank = int(rank)
+        o.local_slab = 1 if local_slab else 0
         self._nccl_id = None
         if nccl_id is not None:
             assert len(nccl_id) == 128
@@ -333,6 +346,52 @@ def nccl_unique_id() -> bytes:
     if st != REACHED:
         raise WcspError(st, last_error())
     return buf.raw
+
+
+def generate_grid(shape, seed: int, lo: int, hi: int, z0: int = 0, z1: int = -1, stream=None):
+    """(f1, f2) of planes [z0, z1) of the last axis as torch uint8 CUDA tensors of shape (d, Nl),
+    generated on the device by wcsp_generate_grid (same values as instances.grid_values)."""
+    import torch
+    d = len(shape)
+    sh = (ctypes.c_int64 * 4)(*[int(x) for x in shape], *([1] * (4 - d)))
+    nL = int(shape[-1])
+    z1 = nL if z1 < 0 else z1
+    Nl = (z1 - z0) * int(np.prod(shape[:-1], dtype=np.int64))
+    f1 = torch.empty((d, Nl), dtype=torch.uint8, device="cuda")
+    f2 = torch.empty((d, Nl), dtype=torch.uint8, device="cuda")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    st = load_library().wcsp_generate_grid(d, sh, int(seed) & ((1 << 64) - 1), int(lo), int(hi), int(z0), int(z1),
+                                           f1.data_ptr(), f2.data_ptr(), s.cuda_stream)
+    if st != REACHED:
+        raise WcspError(st, last_error())
+    return f1, f2
+
+
+def generate_mask(shape, rule: str, z0: int = 0, z1: int = -1, stream=None):
+    """Vertex set `rule` (instances.set_mask rules face0/face1/boundary/centre/corner0/corner1) of
+    planes [z0, z1), as a torch uint8 CUDA tensor, generated by wcsp_generate_mask."""
+    import torch
+    d = len(shape)
+    sh = (ctypes.c_int64 * 4)(*[int(x) for x in shape], *([1] * (4 - d)))
+    nL = int(shape[-1])
+    z1 = nL if z1 < 0 else z1
+    Nl = (z1 - z0) * int(np.prod(shape[:-1], dtype=np.int64))
+    out = torch.empty(Nl, dtype=torch.uint8, device="cuda")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    st = load_library().wcsp_generate_mask(d, sh, SET_RULES[rule], int(z0), int(z1), out.data_ptr(), s.cuda_stream)
+    if st != REACHED:
+        raise WcspError(st, last_error())
+    return out
+
+
+def slab_planes(n_last: int, nranks: int, rank: int):
+    """(z0, z1, p0, p1): slab `rank` owns planes [z0, z1) of the last axis; with
+    Solver(local_slab=True) its arrays cover planes [p0, p1) (ghosts included)."""
+    out = (ctypes.c_int64 * 4)()
+    st = load_library().wcsp_slab_planes(int(n_last), int(nranks), int(rank), out)
+    if st != REACHED:
+        raise WcspError(st, last_error())
+    return tuple(int(x) for x in out)
 
 
 def version() -> str:

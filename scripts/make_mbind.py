@@ -17,6 +17,8 @@ from paper_1511_06441_b200 import instances as I  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "mbind.json")
 SHAPES = {"C2": (1024, 1024), "C3": (256, 256, 256), "C3s": (128, 128, 128), "C5": (1024, 1024, 1024),
+          # one z-slab of C5 at 8 GPUs (1024 x 1024 x 128): the DRAM-resident per-GPU regime
+          "C5z8": (1024, 1024, 128),
           # §6 protocol: water on the cube's boundary, B = the centre vertex
           "P6-50": (50, 50, 50), "P6-75": (75, 75, 75), "P6-100": (100, 100, 100), "P6-125": (125, 125, 125)}
 

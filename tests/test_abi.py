@@ -85,3 +85,21 @@ def test_budget_range_is_validated_before_any_device_work():
             with pytest.raises(wcsp.WcspError) as e:
                 wcsp.solve(I.fixture_B().with_M(ok))
             assert e.value.status == wcsp.ECUDA, ok
+
+
+def test_slab_planes_partition():
+    """wcsp_slab_planes (host arithmetic): the slabs tile the last axis
+    exactly, each holds its neighbours' boundary planes as ghosts, and bad
+    arguments are WCSP_EINVAL."""
+    for n, R in [(1024, 8), (256, 3), (7, 7), (100, 4), (5, 1)]:
+        cover = []
+        for r in range(R):
+            z0, z1, p0, p1 = wcsp.slab_planes(n, R, r)
+            assert z0 == r * n // R and z1 == (r + 1) * n // R and z1 > z0
+            assert p0 == z0 - (r > 0) and p1 == z1 + (r < R - 1)
+            cover += list(range(z0, z1))
+        assert cover == list(range(n))
+    for bad in [(4, 5, 0), (8, 2, 2), (8, 0, 0), (8, 2, -1)]:
+        with pytest.raises(wcsp.WcspError) as e:
+            wcsp.slab_planes(*bad)
+        assert e.value.status == wcsp.EINVAL

@@ -170,10 +170,9 @@ cudaError_t set_smem_attrs() {
 // so a round count just above an integer leaves most warps idle in the last round: take 16
 // words when that gives at most one round or at least four (C2, C3), else 8 (C3s, P6 cubes).
 // WCSP_WIN_WORDS overrides (A/B runs).
-// Interleaved treat rounds (phase_treat): on grids whose vertex state words are several times the
-// L2, every block's round r lies in one chunk of the grid so that the whole device works on one
-// L2-sized chunk of the front at a time (the fire then follows the same order).  WCSP_ILEAVE=0/1
-// overrides (A/B runs).
+// Interleaved treat rounds (phase_treat, build option for A/B runs, WCSP_ILEAVE=1): every block's
+// round r lies in one chunk of the grid so that the whole device treats and fires one L2-sized
+// chunk of the front at a time.  Measured slower than contiguous block slabs on C3 and C5.
 bool ileave_for(const wcsp_handle* h);
 
 unsigned win_words_for(unsigned nwords, unsigned nblocks) {
@@ -184,8 +183,18 @@ unsigned win_words_for(unsigned nwords, unsigned nblocks) {
 }
 
 bool ileave_for(const wcsp_handle* h) {
+  (void)h;
+  // measured slower on C3 (134 -> 161 ms: no block-local bitmap, scattered fire) and on C5 (80.5 ->
+  // 80.0 / 83.5 s): off unless requested (profiles/r02/ab_ileave_*.txt)
   if (const char* e = getenv("WCSP_ILEAVE")) return atoi(e) != 0;
-  return (unsigned long long)h->N * sizeof(unsigned long long) > 2ull * (unsigned long long)h->l2_bytes;
+  return false;
+}
+
+// Fire chunk order (wheel_fire): strided = every block walks its run lists in filing order.
+// WCSP_FIRE_STRIDE=0/1 overrides (A/B runs).
+bool fstride_for(const wcsp_handle* h) {
+  if (const char* e = getenv("WCSP_FIRE_STRIDE")) return atoi(e) != 0;
+  return ileave_for(h);
 }
 
 Dev make_dev(const wcsp_handle* h) {
@@ -239,6 +248,7 @@ Dev make_dev(const wcsp_handle* h) {
   s.nblocks = (unsigned)h->grid;
   s.win_words = win_words_for(s.nwords, s.nblocks);
   s.ileave = ileave_for(h);
+  s.fstride = fstride_for(h);
   s.goff = h->goff;
   s.plane = h->plane;
   s.ghost_hi_start = h->ghi ? h->ghost_hi_start : (unsigned)h->N;
@@ -1369,6 +1379,7 @@ Dev make_peer_dev(wcsp_handle* g, int i) {
   s.nblocks = g->peer_per;
   s.win_words = win_words_for(s.nwords, s.nblocks);
   s.ileave = ileave_for(c);
+  s.fstride = fstride_for(c);
   s.blk0 = dist ? 0u : (unsigned)i * g->peer_per;
   s.plo_end = c->glo ? c->plane : 0u;
   if (dist) {

@@ -54,6 +54,16 @@ constexpr int QA_CAP = 2048;             // shared staging of active-list append
 #define WCSP_WIN_MAX 16
 #endif
 constexpr int WIN_WORDS = WCSP_WIN_MAX;  // max triggered-bitmap words per warp window (Dev.win_words: 8 or 16)
+// Frontier-granularity experiment (SURVEY §8(a) "frontier granularity", build option): stage each
+// treat round's band of vertex state words — the round's 32 * WARPS * ww vertices plus one stride of
+// axis 1 on either side — into shared memory with one TMA bulk copy (cp.async.bulk + mbarrier), so
+// Q's own word and its +-x / +-y neighbour tests read shared memory; +-z stays global.
+#ifndef WCSP_TREAT_STAGE
+#define WCSP_TREAT_STAGE 0
+#endif
+#ifndef WCSP_STAGE_WORDS
+#define WCSP_STAGE_WORDS 4096
+#endif
 constexpr int WIN_VERTS = WIN_WORDS * 32;
 
 constexpr unsigned LBL_REMOVED = 0xFFFFu;  // label of a vertex outside G': no S6 test passes
@@ -154,6 +164,7 @@ struct Dev {
   unsigned nwords;                 // words of the bitmap
   unsigned win_words;              // bitmap words per warp window of the treat (8 or 16)
   unsigned ileave;                 // treat rounds interleaved across blocks (chunk-at-a-time; see phase_treat)
+  unsigned fstride;                // fire: warps take run chunks in turn (list order), see wheel_fire
   unsigned* act[2];
   unsigned long long* pool[2];
   unsigned long long pool_cap;
@@ -386,12 +397,36 @@ struct Smem {
   unsigned long long tphase;       // globaltimer at the start of this block's phase
   unsigned long long red[WARPS][7];
   unsigned redmin[WARPS];
+#if WCSP_TREAT_STAGE
+  alignas(16) unsigned long long stg[WCSP_STAGE_WORDS];   // the round's band of state words
+  unsigned long long stg_bar;      // mbarrier of the bulk copy
+  unsigned stg_lo, stg_n, stg_phase;
+#endif
 };
 
 __device__ __forceinline__ Smem& smem() {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   return *reinterpret_cast<Smem*>(smem_raw);
 }
+
+#if WCSP_TREAT_STAGE
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+// thread 0: stage words [lo, lo + n) of sw into sm.stg (n even, lo even: 16-byte granules)
+__device__ __forceinline__ void stage_issue(const Dev& s, Smem& sm, unsigned lo, unsigned n) {
+  const unsigned bar = smem_u32(&sm.stg_bar), dst = smem_u32(sm.stg), bytes = n * 8u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");    // generic reads of the old band first
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(s.sw + lo), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void stage_wait(Smem& sm, unsigned phase) {
+  const unsigned bar = smem_u32(&sm.stg_bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+}
+#endif
 
 template <class T>
 __device__ __forceinline__ void qpush(T* qbuf, unsigned qcap, unsigned* qn, bool pred, T x, unsigned* gcount,
@@ -924,7 +959,13 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     qpush<unsigned>(sm.qa, QA_CAP, &sm.na, inactive && neww != 0, q, &acc->n_act, s.act[v.cur ^ 1], 0xFFFFFFFFull);
     return;
   }
+#if WCSP_TREAT_STAGE
+  const unsigned slo = sm.stg_lo, sn = sm.stg_n;
+  auto staged = [&](unsigned u) { return u - slo < sn; };
+  const unsigned long long swq = valid ? (staged(q) ? sm.stg[q - slo] : ld_hint(s.sw + q, pol_last())) : 0ull;
+#else
   const unsigned long long swq = valid ? ld_hint(s.sw + q, pol_last()) : 0ull;
+#endif
   const WRec<LW> wr = valid ? load_wt_cs<D>(s, q) : WRec<LW>{0, 0};
   unsigned long long swr[2 * D];
 #if WCSP_TREAT_EAGER
@@ -962,7 +1003,12 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       const Loc L = locate<true>(s, q + s.off[j]);
       swr[j] = test ? (L.sw == s.sw ? s.sw[L.idx] : __ldcv(L.sw + L.idx)) : 0xFFFFull;
     } else {
+#if WCSP_TREAT_STAGE
+      const unsigned u = q + s.off[j];
+      swr[j] = test ? (staged(u) ? sm.stg[u - slo] : s.sw[u]) : 0xFFFFull;
+#else
       swr[j] = test ? s.sw[q + s.off[j]] : 0xFFFFull;   // untested lanes read as "removed"
+#endif
     }
   }
   LW neww = 0;
@@ -1126,7 +1172,28 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
         T += t;
       }
       window_emit(s, bits, base, flat, warp * ww * 32u);
+#if WCSP_TREAT_STAGE
+      if constexpr (!PEER) {
+        if (threadIdx.x == 0) {          // the round's band (+ one axis-1 stride each side), if it fits
+          const unsigned rb = rwin(r) * ww * 32u, H = s.NL >= 4 ? s.off[2] : 1u;
+          const unsigned lo = (rb >= H ? rb - H : 0u) & ~1u;
+          const unsigned hi = (unsigned)min((unsigned long long)s.N, (unsigned long long)rb + ww * 32u * WARPS + H);
+          const unsigned n = (hi - lo + 1u) & ~1u;
+          const bool ok = T > 0 && n <= (unsigned)WCSP_STAGE_WORDS && lo + n <= ((s.N + 1u) & ~1u);
+          sm.stg_lo = lo;
+          sm.stg_n = ok ? min(n, s.N - lo) : 0u;
+          if (ok) stage_issue(s, sm, lo, n);
+        }
+      }
+#endif
       __syncthreads();
+#if WCSP_TREAT_STAGE
+      if constexpr (!PEER) {
+        if (sm.stg_n) { stage_wait(sm, sm.stg_phase & 1u); }
+        __syncthreads();
+        if (threadIdx.x == 0 && sm.stg_n) sm.stg_phase += 1;
+      }
+#endif
 #if WCSP_WIN_PREFETCH
       if (r + 1 < rounds) raw = window_load(s, rwin(r + 1) + warp, nwin);   // next round in flight
 #else
@@ -1339,6 +1406,12 @@ __device__ __forceinline__ void load_view(const Dev& s, Smem& sm, View& v) {
 
 __device__ __forceinline__ void init_smem(Smem& sm) {
   if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; sm.nspill = 0; }
+#if WCSP_TREAT_STAGE
+  if (threadIdx.x == 0) {
+    sm.stg_n = 0; sm.stg_lo = 0; sm.stg_phase = 0;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.stg_bar)) : "memory");
+  }
+#endif
   __syncthreads();
 }
 

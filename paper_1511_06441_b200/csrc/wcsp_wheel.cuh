@@ -369,13 +369,14 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
     const unsigned nchunks = dchunk[n];
     // warp w fires a contiguous range of chunks (the descriptor index then advances by at most
     // one per chunk); the first descriptor is found by binary search over the prefix sums
-    // Interleaved grids (s.ileave): the block's warps take chunks in turn (c = warp, warp + WARPS,
-    // ...), so the whole device walks every run list front to back together and the atomics of a
-    // fire stay inside the L2-sized chunk of the grid the lists were filed from.  Otherwise warp w
-    // fires a contiguous eighth of the list.
-    const unsigned cstep = s.ileave ? (unsigned)WARPS : 1u;
-    const unsigned c_lo = s.ileave ? warp : (unsigned)((unsigned long long)nchunks * warp / WARPS);
-    const unsigned c_hi = s.ileave ? nchunks : (unsigned)((unsigned long long)nchunks * (warp + 1) / WARPS);
+    // s.fstride: the block's warps take chunks in turn (c = warp, warp + WARPS, ...), so every
+    // block walks its run lists front to back — i.e. in the order its treat rounds filed them — and
+    // the whole device fires the events of about one treat round per block at a time (a working set
+    // of ~3 x rounds' state words instead of the whole front).  Otherwise warp w fires a contiguous
+    // eighth of the list.
+    const unsigned cstep = s.fstride ? (unsigned)WARPS : 1u;
+    const unsigned c_lo = s.fstride ? warp : (unsigned)((unsigned long long)nchunks * warp / WARPS);
+    const unsigned c_hi = s.fstride ? nchunks : (unsigned)((unsigned long long)nchunks * (warp + 1) / WARPS);
     unsigned di = 0;
     {
       unsigned lo = 0, hi = n;                   // largest di with dchunk[di] <= c_lo

@@ -72,8 +72,7 @@ struct wcsp_handle {
   unsigned long long ev_cap = 0;
   unsigned long long* bdesc = nullptr;
   unsigned long long* spill = nullptr;               // [grid][spill_cap] staging overflow of the treat
-  unsigned* tlist = nullptr;                         // [grid][QA_CAP] triggered lists of the fire phase
-  unsigned* tcount = nullptr;                        // [grid]
+  unsigned* tlist = nullptr;                         // [grid * QA_CAP] triggered list of a sparse fire phase
   unsigned spill_cap = 0;
   unsigned* bcounts = nullptr;                       // bnev [256] | bnlane [256] | bndesc [256][grid]
   unsigned dcap = 0;
@@ -241,7 +240,6 @@ Dev make_dev(const wcsp_handle* h) {
   s.spill = h->spill;
   s.spill_cap = h->spill_cap;
   s.tlist = h->tlist;
-  s.tcount = h->tcount;
   // sparse cycles: about 64 triggered vertices per block (WCSP_LIST_MAX overrides, A/B runs)
   s.list_max = getenv("WCSP_LIST_MAX") ? strtoull(getenv("WCSP_LIST_MAX"), nullptr, 10)
                                        : (unsigned long long)h->grid * 64ull;
@@ -249,6 +247,7 @@ Dev make_dev(const wcsp_handle* h) {
   s.win_words = win_words_for(s.nwords, s.nblocks);
   s.ileave = ileave_for(h);
   s.fstride = fstride_for(h);
+  s.wbal = getenv("WCSP_WBAL") ? atoi(getenv("WCSP_WBAL")) != 0 : false;   // A/B: neutral on C3, slower on C2
   s.goff = h->goff;
   s.plane = h->plane;
   s.ghost_hi_start = h->ghi ? h->ghost_hi_start : (unsigned)h->N;
@@ -336,7 +335,7 @@ wcsp_status validate_device(wcsp_handle* h, const uint8_t* f1, const uint8_t* f2
     if (h->barr) cudaFree(h->barr);
     h->barr = nullptr;
     h->barr_cap = 0;
-    CK(cudaMalloc(&h->barr, need * sizeof(BArr)));
+    CK(cudaMalloc(&h->barr, 2 * need * sizeof(BArr)));   // one list per cycle parity
     h->barr_cap = (unsigned)need;
   }
   return WCSP_REACHED;
@@ -386,7 +385,7 @@ wcsp_status load_problem(wcsp_handle* h, const wcsp_problem* p) {
     if (need > h->barr_cap) {
       if (h->barr) cudaFree(h->barr);
       h->barr = nullptr;
-      CK(cudaMalloc(&h->barr, need * sizeof(BArr)));
+      CK(cudaMalloc(&h->barr, 2 * need * sizeof(BArr)));
       h->barr_cap = (unsigned)need;
     }
   }
@@ -410,7 +409,7 @@ void release(wcsp_handle* h) {
   void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->lab, h->tbits, h->barr,
                   h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
                   h->d_cnt, h->d_ghost, h->g_out_lo, h->g_out_hi, h->g_in_lo, h->g_in_hi, h->l_out_lo,
-                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl, h->spill, h->tlist, h->tcount};
+                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl, h->spill, h->tlist};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -461,7 +460,6 @@ wcsp_status reset_ctl(wcsp_handle* h) {
   CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
   if (is_wheel(h->eng)) {
     CK(cudaMemsetAsync(h->bcounts, 0, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned), h->stream));
-    CK(cudaMemsetAsync(h->tcount, 0, (size_t)h->grid * sizeof(unsigned), h->stream));
   }
   return WCSP_REACHED;
 }
@@ -550,6 +548,11 @@ int x_lane_of(const wcsp_handle* h, long long X, long long Y) {
 wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
   wcsp_status st;
   h->launches = 0;
+#if WCSP_CHECKS
+  // checked build: poison the event ring (src 0x3F7F7F7F), so an event read before it was written
+  // in this solve traps in the fire's bounds check
+  if (is_wheel(h->eng) && h->ev) CK(cudaMemsetAsync(h->ev, 0x7F, h->ev_cap * sizeof(unsigned long long), h->stream));
+#endif
   CK(cudaEventRecord(h->e0, h->stream));
   if ((st = reset_ctl(h)) != WCSP_REACHED) return st;
   if ((st = launch_init(h)) != WCSP_REACHED) return st;
@@ -763,7 +766,6 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
                                                           std::max<unsigned long long>(2048, pow2_at_least(8 * N / h->grid)));
     CKC(cudaMalloc(&h->spill, (size_t)h->grid * h->spill_cap * sizeof(unsigned long long)));
     CKC(cudaMalloc(&h->tlist, (size_t)h->grid * QA_CAP * sizeof(unsigned)));
-    CKC(cudaMalloc(&h->tcount, (size_t)h->grid * sizeof(unsigned)));
   } else {
     CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
     CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));
@@ -1380,6 +1382,7 @@ Dev make_peer_dev(wcsp_handle* g, int i) {
   s.win_words = win_words_for(s.nwords, s.nblocks);
   s.ileave = ileave_for(c);
   s.fstride = fstride_for(c);
+  s.wbal = getenv("WCSP_WBAL") ? atoi(getenv("WCSP_WBAL")) != 0 : false;   // A/B: neutral on C3, slower on C2
   s.blk0 = dist ? 0u : (unsigned)i * g->peer_per;
   s.plo_end = c->glo ? c->plane : 0u;
   if (dist) {

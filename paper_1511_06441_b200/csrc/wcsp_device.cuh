@@ -30,6 +30,7 @@
 // overwrites, so an arrival learns what D is from the atomic's return value.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -58,6 +59,26 @@ constexpr int WIN_WORDS = WCSP_WIN_MAX;  // max triggered-bitmap words per warp 
 // treat round's band of vertex state words — the round's 32 * WARPS * ww vertices plus one stride of
 // axis 1 on either side — into shared memory with one TMA bulk copy (cp.async.bulk + mbarrier), so
 // Q's own word and its +-x / +-y neighbour tests read shared memory; +-z stays global.
+// Checked build (-DWCSP_CHECKS=1, tests only): device-side bounds checks on every vertex index the
+// fire, treat and sweep derive from a list, bitmap or event record, and a poisoned event ring, so a
+// stale or torn read traps (compute-sanitizer is closed on this pool).
+#ifndef WCSP_CHECKS
+#define WCSP_CHECKS 0
+#endif
+#if WCSP_CHECKS
+#define WCSP_CHECK(cond, what, a, b)                                                              \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("WCSP_CHECK failed: %s (%llu, %llu) block %d thread %d\n", what, (unsigned long long)(a), \
+             (unsigned long long)(b), (int)blockIdx.x, (int)threadIdx.x);                        \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define WCSP_CHECK(cond, what, a, b) do { } while (0)
+#endif
+constexpr unsigned long long EV_POISON = 0x7FFFFFFFFFFFFFFFull;   // src 0x3FFFFFFF: out of range
+
 #ifndef WCSP_TREAT_STAGE
 #define WCSP_TREAT_STAGE 0
 #endif
@@ -94,6 +115,7 @@ struct Acc {                       // per-cycle accumulators, triple-buffered by
   unsigned n_act;                  // entries appended to the next active list
   unsigned n_pool;                 // phantoms appended to the next pool (may exceed capacity)
   unsigned tl_over;                // wheel: first arrivals beyond some block's list went to the bitmap
+  unsigned tl_total;               // wheel, sparse cycles: vertices in the cycle's global triggered list
   unsigned dmin;                   // min live residual after this cycle (0xFFFFFFFF = nothing live)
   unsigned long long bhit;         // max over B arrivals of (cand << 32 | ~X)
   unsigned long long live;         // sweep: live lanes at the top of the cycle (E); wheel: lanes started
@@ -120,7 +142,8 @@ struct Ctl {
   Acc acc[3];
   unsigned long long bar;          // grid barrier arrivals (persistent engines)
   unsigned long long rel;          // peer halo: epoch released by this slab's leader block
-  unsigned abort, n_barr;          // barrier watchdog fired; B-arrival list length
+  unsigned abort, pad1_;           // barrier watchdog fired
+  unsigned n_barr2[2];             // B-arrival list length per cycle parity (list c & 1 at barr[(c & 1) * barr_cap])
   long long F1, F2, X, Y;
   long long via;
   long long cycles, edge_updates, arrivals, triggered, created, relabels, started;
@@ -165,6 +188,7 @@ struct Dev {
   unsigned win_words;              // bitmap words per warp window of the treat (8 or 16)
   unsigned ileave;                 // treat rounds interleaved across blocks (chunk-at-a-time; see phase_treat)
   unsigned fstride;                // fire: warps take run chunks in turn (list order), see wheel_fire
+  unsigned wbal;                   // treat: balanced window slabs per block (block_windows)
   unsigned* act[2];
   unsigned long long* pool[2];
   unsigned long long pool_cap;
@@ -185,8 +209,8 @@ struct Dev {
   unsigned dcap;
   int f1max;
   unsigned long long* spill;       // [nblocks][spill_cap] events past a block's staging, per flush period
-  unsigned* tlist;                 // [nblocks][QA_CAP] wheel: vertices a block's fire triggered (first arrivals)
-  unsigned* tcount;                // [nblocks] their number (> QA_CAP: the rest are in the bitmap)
+  unsigned* tlist;                 // [nblocks * QA_CAP] wheel, sparse cycles: the vertices the fire triggered
+                                   // (first arrivals), appended block by block (acc->tl_total)
   unsigned long long list_max;     // a cycle is sparse (listed) if the previous one triggered at most this many
   unsigned spill_cap;
   unsigned nblocks;                // grid size of the cycle kernels (wheel region sizing)
@@ -575,8 +599,9 @@ __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* ac
       const Loc L = locate<PEER>(s, D);
       const unsigned Dg = L.idx + L.goff;
       atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - Dg));
-      const unsigned k = atomicAdd(&s.ctl->n_barr, 1u);
-      if (k < s.barr_cap) s.barr[k] = BArr{Dg, (unsigned)cand, src, via};
+      const unsigned par = v.c & 1u;
+      const unsigned k = atomicAdd(&s.ctl->n_barr2[par], 1u);
+      if (k < s.barr_cap) s.barr[(size_t)par * s.barr_cap + k] = BArr{Dg, (unsigned)cand, src, via};
     } else if (!PEER && old >= TMP_GHOST) {   // D belongs to a neighbouring slab: hand the water to its owner
       unsigned long long* slot = D < s.plane ? s.ghost_out_lo + D : s.ghost_out_hi + (D - s.ghost_hi_start);
       atomicMax(slot, ((unsigned long long)v.stamp << 48) | ((unsigned long long)(unsigned)cand << 32) |
@@ -617,8 +642,9 @@ __device__ __forceinline__ void arrive_post_w(const Dev& s, const View& v, Acc* 
     if (old == TMPW_B) {           // termination 1°
       const unsigned Dg = D + s.goff;
       atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - Dg));
-      const unsigned k = atomicAdd(&s.ctl->n_barr, 1u);
-      if (k < s.barr_cap) s.barr[k] = BArr{Dg, (unsigned)cand, src, via};
+      const unsigned par = v.c & 1u;
+      const unsigned k = atomicAdd(&s.ctl->n_barr2[par], 1u);
+      if (k < s.barr_cap) s.barr[(size_t)par * s.barr_cap + k] = BArr{Dg, (unsigned)cand, src, via};
     }
   } else if (os != v.stamp) {      // first arrival of the cycle
     atomicOr(s.tbits + (D >> 5), 1u << (D & 31u));
@@ -667,6 +693,7 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
       for (int it = 0; it < SWEEP_ITEMS; ++it) {
         const unsigned i = ch * chunk + it * THREADS + threadIdx.x;
         vx[it] = ((unsigned)it < items && i < v.n_act) ? __ldcg(act_in + i) : 0xFFFFFFFFu;
+        WCSP_CHECK(vx[it] == 0xFFFFFFFFu || vx[it] < s.N, "sweep: active-list entry", vx[it], s.N);
       }
 #pragma unroll
       for (int it = 0; it < SWEEP_ITEMS; ++it) w[it] = vx[it] != 0xFFFFFFFFu ? __ldcg(res + vx[it]) : (LW)0;
@@ -752,6 +779,8 @@ __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
       for (int it = 0; it < SWEEP_ITEMS; ++it) {
         const unsigned i = pc * chunk + it * THREADS + threadIdx.x;
         p[it] = ((unsigned)it < items && i < v.n_pool) ? __ldcs(pool_in + i) : 0ull;
+        WCSP_CHECK(p[it] == 0ull || (((unsigned)p[it] & 0x3FFFFFFFu) < s.N && ((p[it] >> PH_LANE) & 7u) < (unsigned)s.NL),
+                   "sweep: phantom record", p[it], s.N);
       }
       unsigned old[SWEEP_ITEMS];
 #pragma unroll
@@ -911,6 +940,7 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
                                           unsigned& lanes_started, unsigned& tested) {
   using LW = typename Tr<D>::LW;
   const bool valid = q != 0xFFFFFFFFu;
+  WCSP_CHECK(!valid || q < s.N, "treat: vertex index", q, s.N);
   tested += valid;
   if constexpr (W) {
     static_assert(!WHEEL_ENGINE && !PEER, "wide labels: sweep engine, single device");
@@ -1003,6 +1033,7 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       const Loc L = locate<true>(s, q + s.off[j]);
       swr[j] = test ? (L.sw == s.sw ? s.sw[L.idx] : __ldcv(L.sw + L.idx)) : 0xFFFFull;
     } else {
+      WCSP_CHECK(!test || q + s.off[j] < s.N, "treat: neighbour index", q, j);
 #if WCSP_TREAT_STAGE
       const unsigned u = q + s.off[j];
       swr[j] = test ? (staged(u) ? sm.stg[u - slo] : s.sw[u]) : 0xFFFFull;
@@ -1102,22 +1133,49 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
 // Flush hook of the wheel (defined in wcsp_wheel.cuh).
 __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, bool final_flush);
 
+// The treat windows of block vb: [wlo, whi) in `rounds` rounds of WARPS windows (the last may be
+// partial): WARPS * ceil(nwin / (G * WARPS)) windows per block from the start (the tail blocks may
+// get none), or balanced slabs [b * nwin / G, (b + 1) * nwin / G) (s.wbal, A/B option).  The
+// fire's block-local bitmap (wheel_fire) covers the same slab.  ileave: round-robin chunks instead.
+__host__ __device__ __forceinline__ void block_windows(const Dev& s, unsigned vb, unsigned nwin, unsigned& wlo,
+                                                       unsigned& whi, unsigned& rounds) {
+  const unsigned G = s.nblocks;
+  if (s.ileave) {
+    rounds = (nwin + G * WARPS - 1) / (G * WARPS);
+    wlo = 0;
+    whi = nwin;
+  } else if (s.wbal) {
+    wlo = (unsigned)((unsigned long long)nwin * vb / G);
+    whi = (unsigned)((unsigned long long)nwin * (vb + 1) / G);
+    rounds = (whi - wlo + WARPS - 1) / WARPS;
+  } else {
+    const unsigned r0 = (nwin + G * WARPS - 1) / (G * WARPS);
+    wlo = min(nwin, vb * r0 * WARPS);
+    whi = min(nwin, wlo + r0 * WARPS);
+    rounds = r0;
+  }
+}
+
 template <int D, bool WHEEL_ENGINE, bool PEER = false, bool W = false>
 __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   Acc* acc = &s.ctl->acc[v.c % 3];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const unsigned nwin = (s.nwords + s.win_words - 1) / s.win_words;
   // every block owns one contiguous slab of windows: its phantoms / events come from a
-  // compact region of the grid, so a run's destinations share sectors and L2 lines
-  const unsigned rounds = (nwin + s.nblocks * WARPS - 1) / (s.nblocks * WARPS);
+  // compact region of the grid, so a run's destinations share sectors and L2 lines (block_windows;
+  // the balanced split, which gives every block work on C2, measured neutral on C3 and 1.5 % slower
+  // on C2, is an A/B option).
   const unsigned vb = blockIdx.x - s.blk0;
-  const unsigned win0 = vb * rounds * WARPS;
-  // first window of round r: a contiguous slab of windows per block, or (s.ileave, grids whose
-  // state words exceed L2) round r of every block inside one chunk of nblocks * WARPS windows,
-  // so the whole grid treats — and later fires — one L2-sized chunk of the front at a time
-  auto rwin = [&](unsigned r) -> unsigned { return s.ileave ? (r * s.nblocks + vb) * WARPS : win0 + r * WARPS; };
+  unsigned wlo, whi, rounds;
+  block_windows(s, vb, nwin, wlo, whi, rounds);
+  // first window of round r: the block's slab, or (s.ileave, A/B option) round r of every block
+  // inside one chunk of nblocks * WARPS windows
+  auto rwin = [&](unsigned r) -> unsigned { return s.ileave ? (r * s.nblocks + vb) * WARPS : wlo + r * WARPS; };
   unsigned dmin = 0xFFFFFFFFu;
   unsigned created = 0, relabels = 0, triggered = 0, lanes_started = 0, tested = 0;   // per thread, this cycle
+#if WCSP_TREAT_STAGE
+  if (threadIdx.x == 0) sm.stg_n = 0;   // nothing staged until a dense round stages its band
+#endif
   if constexpr (WHEEL_ENGINE) {
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
       sm.rcap[d] = 0; sm.rfill[d] = 0; sm.ofill[d] = 0;
@@ -1132,12 +1190,14 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
   }
   bool scan = true;
   if constexpr (WHEEL_ENGINE) {
-    if (!s.slab && v.lmode) {      // sparse cycle: the vertices this block's fire triggered, then the bitmap if needed
-      const unsigned vb = blockIdx.x - s.blk0;
-      const unsigned cnt = min(__ldcg(s.tcount + vb), (unsigned)QA_CAP);
-      const unsigned* tl = s.tlist + (size_t)vb * QA_CAP;
-      for (unsigned b = warp * 32; b < cnt; b += WARPS * 32) {
-        const unsigned q = b + lane < cnt ? __ldcg(tl + b + lane) : 0xFFFFFFFFu;
+    if (!s.slab && v.lmode) {      // sparse cycle: the cycle's triggered list, then the bitmap if needed
+      // batch k (32 vertices) of the global list goes to warp k / G of block k % G: a thin front's
+      // few hundred or thousand triggered vertices spread over the whole grid of blocks instead of
+      // queueing in the blocks whose fire found them (C4 cycles: one batch latency)
+      const unsigned total = __ldcg(&acc->tl_total);
+      for (unsigned k = warp * s.nblocks + vb; k * 32u < total; k += s.nblocks * WARPS) {
+        const unsigned i = k * 32u + lane;
+        const unsigned q = i < total ? __ldcg(s.tlist + i) : 0xFFFFFFFFu;
         treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
       }
       scan = __ldcg(&acc->tl_over) != 0;
@@ -1152,9 +1212,9 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
     unsigned short* flat = &sm.wl[0][0];
     const unsigned ww = s.win_words;
 #if WCSP_WIN_PREFETCH
-    unsigned raw = scan && rounds > 0 ? window_load(s, rwin(0) + warp, nwin) : 0u;
+    unsigned raw = scan && rounds > 0 ? window_load(s, rwin(0) + warp, whi) : 0u;
 #else
-    unsigned bits = scan && rounds > 0 ? window_bits(s, rwin(0) + warp, nwin) : 0u;
+    unsigned bits = scan && rounds > 0 ? window_bits(s, rwin(0) + warp, whi) : 0u;
 #endif
     for (unsigned r = 0; scan && r < rounds; ++r) {
 #if WCSP_WIN_PREFETCH
@@ -1195,9 +1255,9 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
       }
 #endif
 #if WCSP_WIN_PREFETCH
-      if (r + 1 < rounds) raw = window_load(s, rwin(r + 1) + warp, nwin);   // next round in flight
+      if (r + 1 < rounds) raw = window_load(s, rwin(r + 1) + warp, whi);   // next round in flight
 #else
-      if (r + 1 < rounds) bits = window_bits(s, rwin(r + 1) + warp, nwin);
+      if (r + 1 < rounds) bits = window_bits(s, rwin(r + 1) + warp, whi);
 #endif
       const unsigned rbase = rwin(r) * ww * 32u;
       for (unsigned b = warp * 32; b < T; b += WARPS * 32) {
@@ -1210,7 +1270,7 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
 #endif
   for (unsigned r = 0; scan && r < rounds; ++r) {
     const unsigned win = rwin(r) + warp;
-    const unsigned total = win < nwin ? window_take(s, win, sm.wl[warp]) : 0u;
+    const unsigned total = win < whi ? window_take(s, win, sm.wl[warp]) : 0u;
     for (unsigned b = 0; b < total; b += 32) {
       const unsigned q = b + lane < total ? win * s.win_words * 32u + sm.wl[warp][b + lane] : 0xFFFFFFFFu;
       treat_one<D, WHEEL_ENGINE, PEER, W>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
@@ -1245,20 +1305,21 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
 // decide (sweep engine): Step 6 + time skipping.  One thread; writes ctl if writer.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void reset_acc(Acc* a) {
-  a->n_act = 0; a->n_pool = 0; a->tl_over = 0; a->dmin = 0xFFFFFFFFu;
+  a->n_act = 0; a->n_pool = 0; a->tl_over = 0; a->tl_total = 0; a->dmin = 0xFFFFFFFFu;
   a->bhit = 0; a->live = 0; a->arrivals = 0; a->created = 0; a->relabels = 0; a->triggered = 0;
   a->started = 0; a->tested = 0; a->pend_lanes = 0; a->pend_phantoms = 0;
 }
 
-__device__ __forceinline__ void resolve_hit(const Dev& s, unsigned long long bhit, long long t) {
+__device__ __forceinline__ void resolve_hit(const Dev& s, unsigned long long bhit, long long t, unsigned c) {
   Ctl* C = s.ctl;
   const unsigned q = (unsigned)(bhit >> 32);
   const unsigned X = 0xFFFFFFFFu - (unsigned)bhit;
-  // Y = smallest source among the arrivals at X carrying q; a regular edge wins over a phantom (R5)
-  const unsigned nb = min(__ldcg(&C->n_barr), s.barr_cap);
+  // Y = smallest source among cycle c's arrivals at X carrying q; a regular edge wins over a phantom (R5)
+  const unsigned par = c & 1u;
+  const unsigned nb = min(__ldcg(&C->n_barr2[par]), s.barr_cap);
   unsigned long long best = ~0ull;
   for (unsigned k = 0; k < nb; ++k) {
-    const BArr b = s.barr[k];
+    const BArr b = s.barr[(size_t)par * s.barr_cap + k];
     if (b.D == X && b.cand == q) best = min(best, ((unsigned long long)b.src << 1) | b.via);
   }
   C->F1 = t;
@@ -1295,7 +1356,7 @@ __device__ void decide(const Dev& s, View& v, bool writer) {
   }
   if (bhit) {
     nv.status = 0;  // WCSP_REACHED
-    if (writer) resolve_hit(s, bhit, v.t);
+    if (writer) resolve_hit(s, bhit, v.t, v.c);
   } else if (n_pool > s.pool_cap) {
     nv.status = 8;  // WCSP_EOVERFLOW
     if (writer) C->need_pool = n_pool;

@@ -280,7 +280,10 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
 __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
   reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
   s.ctl->ts0 = globaltimer_ns();
-  if (s.staircase) s.ctl->n_barr = 0;   // staircase: target arrivals are resolved per cycle
+  // staircase: target arrivals are resolved per cycle; the list of the previous cycle's parity (read by
+  // its decide, which this thread ran) is emptied for the next cycle — the fires of THIS cycle, which
+  // other blocks may already have started, append to the other parity's list
+  if (s.staircase) s.ctl->n_barr2[(v.c + 1) & 1] = 0;
   unsigned long long* nf = &s.ctl->fin[(v.c + 1) & 1][0][0];
   nf[0] = 0; nf[1] = 0; nf[2] = 0; nf[3] = 0;
   const unsigned prev = (unsigned)((v.t - v.delta) & (WHEEL - 1));   // the bucket fired last cycle
@@ -319,11 +322,11 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   const bool redmode = local_bits;
   if (local_bits) {
     if (threadIdx.x == 0) {
-      const unsigned long long ww = s.win_words, nwin = (s.nwords + ww - 1) / ww;
-      const unsigned long long rounds = (nwin + (unsigned long long)s.nblocks * WARPS - 1) / ((unsigned long long)s.nblocks * WARPS);
-      const unsigned long long span = rounds * WARPS * ww * 32ull;
-      const unsigned long long vlo = (unsigned long long)(blockIdx.x - s.blk0) * span;
-      const unsigned long long vhi = min((unsigned long long)s.N, vlo + span);
+      const unsigned long long ww = s.win_words;
+      unsigned wlo, whi, rounds;
+      block_windows(s, blockIdx.x - s.blk0, (unsigned)((s.nwords + ww - 1) / ww), wlo, whi, rounds);
+      const unsigned long long vlo = (unsigned long long)wlo * ww * 32ull;
+      const unsigned long long vhi = min((unsigned long long)s.N, (unsigned long long)whi * ww * 32ull);
       const unsigned long long S = s.off[s.NL - 2], cap = (unsigned long long)QP_CAP * 64ull;
       unsigned long long lo = vlo >= S ? vlo - S : 0ull, hi = min((unsigned long long)s.N, vhi + S);
       if (PEER) {                  // never a ghost plane: those are the neighbours' vertices
@@ -413,6 +416,8 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
         arr += valid;
         const unsigned src = (unsigned)e[it] & 0x3FFFFFFFu;
         const unsigned ln = (unsigned)(e[it] >> PH_LANE) & 7u;
+        WCSP_CHECK(!valid || (src < s.N && ln < (unsigned)s.NL && src + s.off[ln] < s.N), "fire: event record",
+                   e[it], s.N);
 #if WCSP_FIRE_RED
         if constexpr (PEER) {
 #if WCSP_FIRE_RED_PEER
@@ -482,12 +487,13 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
   if constexpr (!PEER) {            // publish the block's triggered list for its treat (sparse cycles)
     if (!s.slab && v.lmode) {
       __syncthreads();
-      const unsigned n = sm.na, m = min(n, (unsigned)QA_CAP), vb = blockIdx.x - s.blk0;
-      for (unsigned i = threadIdx.x; i < m; i += THREADS) s.tlist[(size_t)vb * QA_CAP + i] = sm.qa[i];
+      const unsigned n = sm.na, m = min(n, (unsigned)QA_CAP);
       if (threadIdx.x == 0) {
-        s.tcount[vb] = m;
+        sm.base_a = m ? atomicAdd(&acc->tl_total, m) : 0u;   // sum over blocks <= nblocks * QA_CAP
         if (n > m) atomicOr(&acc->tl_over, 1u);
       }
+      __syncthreads();
+      for (unsigned i = threadIdx.x; i < m; i += THREADS) s.tlist[(size_t)sm.base_a + i] = sm.qa[i];
     }
   }
   block_reduce_commit(sm, 0xFFFFFFFFu, 0, arr, 0, 0, 0, acc);   // (ends with a block barrier:
@@ -628,7 +634,7 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gex
   if (G.bhit && s.staircase) {
     const long long q = (long long)((unsigned long long)G.bhit >> 32);
     if (writer && q > C->stair_q) {
-      resolve_hit(s, (unsigned long long)G.bhit, v.t);
+      resolve_hit(s, (unsigned long long)G.bhit, v.t, v.c);
       const unsigned k = C->n_stair;
       if (k < s.stair_cap) {
         s.stair[4 * k] = v.t;
@@ -643,7 +649,7 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gex
   }
   if (hit_stop) {
     nv.status = 0;
-    if (writer && !s.staircase) resolve_hit(s, (unsigned long long)G.bhit, v.t);
+    if (writer && !s.staircase) resolve_hit(s, (unsigned long long)G.bhit, v.t, v.c);
   } else if (G.overflow) {
     nv.status = 8;  // WCSP_EOVERFLOW: the host grows the event ring / descriptor table and re-runs
     if (writer) C->need_pool = need;

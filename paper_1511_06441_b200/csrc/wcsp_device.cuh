@@ -412,6 +412,7 @@ struct Smem {
   int rlock[WHEEL];
 #endif
   unsigned wtot[WARPS];            // treat, shared rounds: triggered vertices per warp window
+  unsigned claim;                  // treat, shared rounds: next unclaimed 32-vertex batch (WCSP_CLAIM)
   unsigned na, np, nspill;
   unsigned bm_lo, bm_words;        // wheel fire, dense cycles: the block's triggered bitmap in qp covers
                                    // vertices [bm_lo, bm_lo + 32 * bm_words)
@@ -920,6 +921,9 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #ifndef WCSP_WIN_PREFETCH
 #define WCSP_WIN_PREFETCH 0        // 1: the next round's bitmap words load while this round is treated (no gain; off)
 #endif
+#ifndef WCSP_CLAIM
+#define WCSP_CLAIM 1               // warps claim a round's 32-vertex batches dynamically (not round-robin)
+#endif
 #ifndef WCSP_TREAT_AGG
 #define WCSP_TREAT_AGG 1           // one warp-scan staging reservation per treat batch (not one per lane direction)
 #endif
@@ -1232,6 +1236,9 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
         T += t;
       }
       window_emit(s, bits, base, flat, warp * ww * 32u);
+#if WCSP_CLAIM
+      if (threadIdx.x == 0) sm.claim = WARPS * 32u;   // batch w goes to warp w first, then first come
+#endif
 #if WCSP_TREAT_STAGE
       if constexpr (!PEER) {
         if (threadIdx.x == 0) {          // the round's band (+ one axis-1 stride each side), if it fits
@@ -1260,10 +1267,22 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
       if (r + 1 < rounds) bits = window_bits(s, rwin(r + 1) + warp, whi);
 #endif
       const unsigned rbase = rwin(r) * ww * 32u;
+#if WCSP_CLAIM
+      // a warp that finishes its batch takes the next unclaimed one (shared-memory counter), so the
+      // round ends when the work does rather than when the unluckiest warp's fixed share does
+      for (unsigned b = warp * 32; b < T;) {
+        const unsigned q = b + lane < T ? rbase + flat[b + lane] : 0xFFFFFFFFu;
+        treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
+        unsigned nb = 0;
+        if (lane == 0) nb = atomicAdd(&sm.claim, 32u);
+        b = __shfl_sync(0xFFFFFFFFu, nb, 0);
+      }
+#else
       for (unsigned b = warp * 32; b < T; b += WARPS * 32) {
         const unsigned q = b + lane < T ? rbase + flat[b + lane] : 0xFFFFFFFFu;
         treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
       }
+#endif
     }
     scan = false;
   }

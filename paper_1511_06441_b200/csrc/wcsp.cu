@@ -419,14 +419,15 @@ void release(wcsp_handle* h) {
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
 }
 
-// Keep the vertex state words (the atomics' targets and the neighbour tests'
-// reads) resident in L2: an access-policy window on the solver's stream marks
-// up to the device's persisting set-aside as evict-last; streaming traffic
-// (events, weight records) uses evict-first hints in the kernels.  Disabled
-// with WCSP_L2_PERSIST=0.
+// Optional (WCSP_L2_PERSIST=1): an access-policy window on the solver's stream marking up to the
+// device's persisting set-aside of the vertex state words as persisting.  Off by default: the
+// per-access cache-policy hints of the kernels (evict-last on state words, evict-first on events
+// and weight records) already keep the state words resident, and the set-aside only shrinks the
+// L2 the rest competes for — C3 133.8 -> 131.6 ms, C3s 15.08 -> 14.48 ms, C2 96.2 -> 95.4 ms,
+// C5z8 8.75 -> 8.60 s without it (profiles/r02/ab_persist.txt, ab_c5z8_l2.txt).
 void set_l2_window(wcsp_handle* h) {
   const char* env = getenv("WCSP_L2_PERSIST");
-  if (env && env[0] == '0') return;
+  if (!env || env[0] != '1') return;
   int max_persist = 0, max_window = 0;
   if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->dev) != cudaSuccess ||

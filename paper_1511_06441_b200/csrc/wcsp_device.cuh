@@ -922,7 +922,10 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #define WCSP_WIN_PREFETCH 0        // 1: the next round's bitmap words load while this round is treated (no gain; off)
 #endif
 #ifndef WCSP_CLAIM
-#define WCSP_CLAIM 1               // warps claim a round's 32-vertex batches dynamically (not round-robin)
+#define WCSP_CLAIM 0               // 1: warps claim a round's batches dynamically (measured: C3 +0.6 %, C2 +1.8 %; off)
+#endif
+#ifndef WCSP_TREAT_PF
+#define WCSP_TREAT_PF 0            // 1: prefetch the next batch's state word (L2) and weight record (L1)
 #endif
 #ifndef WCSP_TREAT_AGG
 #define WCSP_TREAT_AGG 1           // one warp-scan staging reservation per treat batch (not one per lane direction)
@@ -1280,6 +1283,17 @@ __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
 #else
       for (unsigned b = warp * 32; b < T; b += WARPS * 32) {
         const unsigned q = b + lane < T ? rbase + flat[b + lane] : 0xFFFFFFFFu;
+#if WCSP_TREAT_PF
+        {   // the warp's next batch: its first dependent loads start now, one batch ahead
+          const unsigned bn = b + WARPS * 32 + lane;
+          if (bn < T) {
+            const unsigned qn = rbase + flat[bn];
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(s.sw + qn));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(s.wt) +
+                                                      (size_t)qn * 2 * sizeof(typename Tr<D>::LW)));
+          }
+        }
+#endif
         treat_one<D, WHEEL_ENGINE, PEER>(s, v, sm, acc, q, dmin, created, relabels, triggered, lanes_started, tested);
       }
 #endif

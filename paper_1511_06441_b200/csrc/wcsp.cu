@@ -92,6 +92,10 @@ struct wcsp_handle {
   unsigned* lab = nullptr;                           // [N] u32 labels (allocated on the first wide solve)
   int pool_rec = 8;                                  // bytes per phantom record in pool[] (16: wide)
   int grid_wide = 0;
+  // one-barrier hybrid wheel kernel (k_wheel_hybrid): per-block treat progress, neighbourhood radius
+  bool hyb = false;
+  unsigned long long* prog = nullptr;
+  int hyb_R = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
   long long last_cycles = 0;
   long long launches = 0;
@@ -154,7 +158,8 @@ cudaError_t set_smem_attrs() {
                  reinterpret_cast<void*>(&k_wheel_fire<D>), reinterpret_cast<void*>(&k_wheel_treat<D>),
                  reinterpret_cast<void*>(&k_wheel_peer<D, 3>), reinterpret_cast<void*>(&k_wheel_peer<D, 4>),
                  reinterpret_cast<void*>(&k_persistent<D, true>), reinterpret_cast<void*>(&k_sweep<D, true>),
-                 reinterpret_cast<void*>(&k_treat<D, true>)};
+                 reinterpret_cast<void*>(&k_treat<D, true>), reinterpret_cast<void*>(&k_wheel_hybrid<D, 3>),
+                 reinterpret_cast<void*>(&k_wheel_hybrid<D, 4>)};
   const char* co = getenv("WCSP_CARVEOUT");       // A/B runs: shared-memory carveout in percent of L1
   for (void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -240,6 +245,8 @@ Dev make_dev(const wcsp_handle* h) {
   s.spill = h->spill;
   s.spill_cap = h->spill_cap;
   s.tlist = h->tlist;
+  s.prog = h->prog;
+  s.hyb_R = h->hyb_R;
   // sparse cycles: about 64 triggered vertices per block (WCSP_LIST_MAX overrides, A/B runs)
   s.list_max = getenv("WCSP_LIST_MAX") ? strtoull(getenv("WCSP_LIST_MAX"), nullptr, 10)
                                        : (unsigned long long)h->grid * 64ull;
@@ -409,7 +416,7 @@ void release(wcsp_handle* h) {
   void* bufs[] = {h->d_f1, h->d_f2, h->d_maskA, h->d_maskB, h->d_present, h->wt, h->res, h->sw, h->lab, h->tbits, h->barr,
                   h->act[0], h->act[1], h->pool[0], h->pool[1], h->ev, h->bdesc, h->bcounts, h->ctl, h->trace,
                   h->d_cnt, h->d_ghost, h->g_out_lo, h->g_out_hi, h->g_in_lo, h->g_in_hi, h->l_out_lo,
-                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl, h->spill, h->tlist};
+                  h->l_out_hi, h->l_in_lo, h->l_in_hi, h->d_ctls, h->stair, h->xbar, h->d_pctl, h->spill, h->tlist, h->prog};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -456,11 +463,12 @@ wcsp_status reset_ctl(wcsp_handle* h) {
   c.view.stamp = stamp_of(0);
   c.view.status = ST_RUNNING;
   c.view.region = 256;
-  for (int i = 0; i < 3; ++i) c.acc[i].dmin = 0xFFFFFFFFu;
+  for (int i = 0; i < NACC; ++i) c.acc[i].dmin = 0xFFFFFFFFu;
   c.acc[0].tl_over = 1;            // cycle 0 treats A from the bitmap (k_init)
   CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
   if (is_wheel(h->eng)) {
     CK(cudaMemsetAsync(h->bcounts, 0, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned), h->stream));
+    if (h->prog) CK(cudaMemsetAsync(h->prog, 0, (size_t)h->grid * sizeof(unsigned long long), h->stream));
   }
   return WCSP_REACHED;
 }
@@ -475,10 +483,19 @@ wcsp_status launch_init(wcsp_handle* h) {
   return WCSP_REACHED;
 }
 
+template <int D>
+void* hybrid_fn(bool big) {
+  return big ? reinterpret_cast<void*>(&k_wheel_hybrid<D, 4>) : reinterpret_cast<void*>(&k_wheel_hybrid<D, 3>);
+}
+void* hybrid_fn_d(int d, bool big) {
+  return d == 1 ? hybrid_fn<1>(big) : d == 2 ? hybrid_fn<2>(big) : d == 3 ? hybrid_fn<3>(big) : hybrid_fn<4>(big);
+}
+
 wcsp_status run_persistent(wcsp_handle* h) {
   Dev s = make_dev(h);
   void* args[] = {&s};
-  CK(cudaLaunchCooperativeKernel(cycle_fn_d(h->d, h->eng, h->big, h->wide), dim3(h->grid), dim3(THREADS), args, sizeof(Smem),
+  void* fn = h->hyb ? hybrid_fn_d(h->d, h->big) : cycle_fn_d(h->d, h->eng, h->big, h->wide);
+  CK(cudaLaunchCooperativeKernel(fn, dim3(h->grid), dim3(THREADS), args, sizeof(Smem),
                                  h->stream));
   h->launches += 1;
   return WCSP_REACHED;
@@ -604,18 +621,42 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
 // needed (the front keeps growing), so a retry takes twice that and at least 4x the old size
 // (2x once the structure is past 2^26 entries, where memory matters).
 constexpr int MAX_ATTEMPTS = 12;
+#ifndef HYBRID_DEFAULT
+#define HYBRID_DEFAULT false
+#endif
 unsigned long long grown(unsigned long long cap, long long need) {
   const unsigned long long f = cap < (1ull << 26) ? 4 : 2;
   return std::max<unsigned long long>(2ull * (unsigned long long)std::max(need, 0ll), f * cap);
+}
+
+// The one-barrier hybrid kernel (k_wheel_hybrid) for single-device persistent wheel solves; its
+// neighbourhood radius in blocks covers twice the largest lane offset (a fire's destinations are one
+// offset from its sources, a treat's neighbour reads one offset from its vertices).  WCSP_HYBRID=0/1.
+bool hybrid_for(wcsp_handle* h) {
+  const char* e = getenv("WCSP_HYBRID");
+  const bool want = e ? atoi(e) != 0 : HYBRID_DEFAULT;
+  if (!want || h->eng != WCSP_ENGINE_WHEEL || h->slab_index >= 0 || h->staircase || h->f1max >= 128 || !h->prog)
+    return false;
+  const Dev s = make_dev(h);
+  if (s.ileave || s.wbal) return false;
+  const unsigned long long ww = s.win_words, nwin = (s.nwords + ww - 1) / ww;
+  const unsigned long long r0 = (nwin + (unsigned long long)h->grid * WARPS - 1) / ((unsigned long long)h->grid * WARPS);
+  const unsigned long long span = std::max<unsigned long long>(1, r0 * WARPS * ww * 32ull);
+  unsigned long long maxoff = 1;
+  for (int k = 0; k + 1 < h->d; ++k) maxoff *= (unsigned long long)h->shape[k];
+  h->hyb_R = (int)std::min<unsigned long long>((2 * maxoff + span - 1) / span + 1, (unsigned long long)h->grid);
+  return true;
 }
 
 // Budgets above WCSP_M_MAX run the sweep engine with u32 labels and u64 stamped temps
 // (include/wcsp.h; the 16-bit layout stays the default): allocate its state on first use.
 wcsp_status prepare_engine(wcsp_handle* h) {
   h->wide = wide_M(h->M);
+  h->hyb = false;
   if (!h->wide) {
     h->eng = h->opt.engine;
     h->grid = h->grid_main;
+    h->hyb = hybrid_for(h);
     return WCSP_REACHED;
   }
   h->eng = is_stepped(h->opt.engine) ? WCSP_ENGINE_STEPPED : WCSP_ENGINE_PERSISTENT;
@@ -767,6 +808,7 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
                                                           std::max<unsigned long long>(2048, pow2_at_least(8 * N / h->grid)));
     CKC(cudaMalloc(&h->spill, (size_t)h->grid * h->spill_cap * sizeof(unsigned long long)));
     CKC(cudaMalloc(&h->tlist, (size_t)h->grid * QA_CAP * sizeof(unsigned)));
+    CKC(cudaMalloc(&h->prog, (size_t)h->grid * sizeof(unsigned long long)));
   } else {
     CKC(cudaMalloc(&h->res, N * lane_bytes(h->d)));
     CKC(cudaMalloc(&h->act[0], N * sizeof(unsigned)));

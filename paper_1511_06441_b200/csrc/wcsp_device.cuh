@@ -111,7 +111,11 @@ constexpr int WHEEL = 256;                 // timing wheel buckets (f1 <= 255)
 
 struct BArr { unsigned D, cand, src, via; };   // an arrival at a target (terminating cycle only)
 
-struct Acc {                       // per-cycle accumulators, triple-buffered by cycle % 3
+// Per-cycle accumulators live in NACC slots (slot c % NACC).  The two-barrier kernels need three
+// (the next cycle's slot is reset while this one is read); the one-barrier hybrid kernel reads a
+// cycle's fire half and the previous cycle's treat half in the same decision, so it needs four.
+constexpr int NACC = 4;
+struct Acc {                       // per-cycle accumulators, slot c % NACC
   unsigned n_act;                  // entries appended to the next active list
   unsigned n_pool;                 // phantoms appended to the next pool (may exceed capacity)
   unsigned tl_over;                // wheel: first arrivals beyond some block's list went to the bitmap
@@ -135,11 +139,13 @@ struct View {                      // cycle state every block needs
   int cur, status;
   unsigned region;                 // timing wheel: ring region size per (block, delay)
   unsigned lmode;                  // timing wheel: sparse cycle, fire lists the vertices it triggers
+  unsigned ncount;                 // hybrid kernel: counted (non-empty) cycles so far
+  unsigned pad_;                   // hybrid kernel: the previous cycle was counted
 };
 
 struct Ctl {
   View view;
-  Acc acc[3];
+  Acc acc[NACC];                   // per-cycle accumulators, slot c % NACC
   unsigned long long bar;          // grid barrier arrivals (persistent engines)
   unsigned long long rel;          // peer halo: epoch released by this slab's leader block
   unsigned abort, pad1_;           // barrier watchdog fired
@@ -214,6 +220,10 @@ struct Dev {
   unsigned long long list_max;     // a cycle is sparse (listed) if the previous one triggered at most this many
   unsigned spill_cap;
   unsigned nblocks;                // grid size of the cycle kernels (wheel region sizing)
+  // one-barrier hybrid kernel (k_wheel_hybrid): per-block treat progress and the block radius
+  // within which blocks' fires and treats touch the same state words
+  unsigned long long* prog;        // [nblocks] treats completed (monotone per solve)
+  int hyb_R;
   // slab partition (multi-GPU / virtual slabs): local index + goff = global index
   unsigned goff;
   unsigned plane;                  // vertices per plane of the partitioned (last) axis
@@ -368,16 +378,35 @@ template <int D> __device__ __forceinline__ WRec<typename Tr<D>::LW> load_wt(con
 }
 // streaming variant (evict-first): weight records of triggered vertices are
 // read once per cycle and must not push the vertex state words out of L2
+// (WCSP_WT_POLICY = 1: normal caching, 2: evict-last — A/B options)
+#ifndef WCSP_WT_POLICY
+#define WCSP_WT_POLICY 0
+#endif
 template <int D> __device__ __forceinline__ WRec<typename Tr<D>::LW> load_wt_cs(const Dev& s, unsigned v) {
   using LW = typename Tr<D>::LW;
   WRec<LW> r;
   if constexpr (sizeof(LW) == 4) {
+#if WCSP_WT_POLICY == 0
     uint2 q = __ldcs(reinterpret_cast<const uint2*>(s.wt) + v);
+#else
+    uint2 q = __ldcg(reinterpret_cast<const uint2*>(s.wt) + v);
+#endif
     r.f1 = q.x; r.f2 = q.y;
   } else {
+#if WCSP_WT_POLICY == 0
     uint4 q = __ldcs(reinterpret_cast<const uint4*>(s.wt) + v);
     r.f1 = ((unsigned long long)q.y << 32) | q.x;
     r.f2 = ((unsigned long long)q.w << 32) | q.z;
+#elif WCSP_WT_POLICY == 1
+    uint4 q = __ldcg(reinterpret_cast<const uint4*>(s.wt) + v);
+    r.f1 = ((unsigned long long)q.y << 32) | q.x;
+    r.f2 = ((unsigned long long)q.w << 32) | q.z;
+#else
+    unsigned long long a, b;
+    asm volatile("ld.global.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;"
+                 : "=l"(a), "=l"(b) : "l"(reinterpret_cast<const unsigned long long*>(s.wt) + 2 * (size_t)v), "l"(pol_last()));
+    r.f1 = a; r.f2 = b;
+#endif
   }
   return r;
 }
@@ -416,7 +445,8 @@ struct Smem {
   unsigned na, np, nspill;
   unsigned bm_lo, bm_words;        // wheel fire, dense cycles: the block's triggered bitmap in qp covers
                                    // vertices [bm_lo, bm_lo + 32 * bm_words)
-  unsigned base_a, base_b, flag;
+  unsigned base_a, base_b, flag, ovf;
+  unsigned long long alloc_lim;    // event-ring allocations of this treat must stay below (hybrid guard)
   View view;
   unsigned long long bhit;
   unsigned long long tphase;       // globaltimer at the start of this block's phase
@@ -670,7 +700,7 @@ __device__ __forceinline__ void arrive_p(const Dev& s, const View& v, Acc* acc, 
 template <int D, bool W = false>
 __device__ void phase_sweep(const Dev& s, const View& v, Smem& sm) {
   using LW = typename Tr<D>::LW;
-  Acc* acc = &s.ctl->acc[v.c % 3];
+  Acc* acc = &s.ctl->acc[v.c % NACC];
   LW* res = reinterpret_cast<LW*>(s.res);
   const unsigned* act_in = s.act[v.cur];
   unsigned* act_out = s.act[v.cur ^ 1];
@@ -1165,7 +1195,7 @@ __host__ __device__ __forceinline__ void block_windows(const Dev& s, unsigned vb
 
 template <int D, bool WHEEL_ENGINE, bool PEER = false, bool W = false>
 __device__ void phase_treat(const Dev& s, const View& v, Smem& sm) {
-  Acc* acc = &s.ctl->acc[v.c % 3];
+  Acc* acc = &s.ctl->acc[v.c % NACC];
   const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const unsigned nwin = (s.nwords + s.win_words - 1) / s.win_words;
   // every block owns one contiguous slab of windows: its phantoms / events come from a
@@ -1364,7 +1394,7 @@ __device__ __forceinline__ void resolve_hit(const Dev& s, unsigned long long bhi
 }
 
 __device__ void decide(const Dev& s, View& v, bool writer) {
-  Acc* a = &s.ctl->acc[v.c % 3];
+  Acc* a = &s.ctl->acc[v.c % NACC];
   const unsigned long long bhit = __ldcg(&a->bhit);
   const unsigned n_act = __ldcg(&a->n_act), n_pool = __ldcg(&a->n_pool), dmin = __ldcg(&a->dmin);
   View nv = v;
@@ -1492,6 +1522,7 @@ __device__ __forceinline__ void load_view(const Dev& s, Smem& sm, View& v) {
     View x;
     x.t = g->t; x.c = g->c; x.stamp = g->stamp; x.delta = g->delta; x.n_act = g->n_act;
     x.n_pool = g->n_pool; x.cur = g->cur; x.status = g->status; x.region = g->region; x.lmode = g->lmode;
+    x.ncount = g->ncount; x.pad_ = g->pad_;
     sm.view = x;
   }
   __syncthreads();
@@ -1499,7 +1530,7 @@ __device__ __forceinline__ void load_view(const Dev& s, Smem& sm, View& v) {
 }
 
 __device__ __forceinline__ void init_smem(Smem& sm) {
-  if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; sm.nspill = 0; }
+  if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; sm.nspill = 0; sm.ovf = 0; sm.alloc_lim = ~0ull; }
 #if WCSP_TREAT_STAGE
   if (threadIdx.x == 0) {
     sm.stg_n = 0; sm.stg_lo = 0; sm.stg_phase = 0;
@@ -1538,7 +1569,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_persistent(Dev s) 
   while (v.status == ST_RUNNING) {
     if (v.c > 0) {
       if (blockIdx.x == 0 && threadIdx.x == 0) {
-        reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
+        reset_acc(&s.ctl->acc[(v.c + 1) % NACC]);
         s.ctl->ts0 = globaltimer_ns();
       }
       phase_sweep<D, W>(s, v, sm);
@@ -1546,7 +1577,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_persistent(Dev s) 
       if (!grid_sync(s.ctl, target, sm)) return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
-    if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
+    if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % NACC].bhit);
     __syncthreads();
     const unsigned long long bhit = sm.bhit;
     __syncthreads();
@@ -1579,7 +1610,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_sweep(Dev s) {
   load_view(s, sm, v);
   if (v.status != ST_RUNNING || v.c == 0) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
+    reset_acc(&s.ctl->acc[(v.c + 1) % NACC]);
     s.ctl->ts0 = globaltimer_ns();
   }
   phase_sweep<D, W>(s, v, sm);
@@ -1593,7 +1624,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB_SWEEP) k_treat(Dev s) {
   load_view(s, sm, v);
   if (v.status != ST_RUNNING) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
-  if (__ldcg(&s.ctl->acc[v.c % 3].bhit)) return;
+  if (__ldcg(&s.ctl->acc[v.c % NACC].bhit)) return;
   phase_treat<D, false, false, W>(s, v, sm);
 }
 

@@ -79,6 +79,7 @@ __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long lon
   // rcap and rpos do not change between flushes; the next flush adopts the appended events) ...
   const unsigned k = atomicAdd(&sm.ofill[delay], 1u);
   if (k < sm.rcap[delay] - sm.rfill[delay]) {
+    if (sm.ovf) return;                // the open region lies past the hybrid guard: drop (run retried)
     const unsigned b = (unsigned)((t + delay) & (WHEEL - 1));
     st_hint(s.ev + ((sm.rpos[delay] + sm.rfill[delay] + k) & s.ev_mask), rec, pol_first());
     atomicAdd(s.bnev + b, 1u);
@@ -90,6 +91,7 @@ __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long lon
     s.spill[(size_t)(blockIdx.x - s.blk0) * s.spill_cap + ks] = rec | ((unsigned long long)delay << EV_DELAY_SHIFT);
   } else {                          // ... else file the event as a run of one (rare)
     const unsigned long long pos = atomicAdd(&s.ctl->ev_head, 1ull);
+    if (pos + 1 > sm.alloc_lim) { sm.ovf = 1; atomicOr(&s.ctl->wheel_overflow, 4u); return; }
     s.ev[pos & s.ev_mask] = rec;
     const unsigned b = (unsigned)((t + delay) & (WHEEL - 1));
     atomicAdd(s.bnev + b, 1u);
@@ -217,6 +219,10 @@ __device__ void flush_sorted(const Dev& s, Smem& sm, long long t, unsigned regio
         sm.rpos[d] = atomicAdd(&s.ctl->ev_head, (unsigned long long)size);
         sm.rfill[d] = 0;
         sm.rcap[d] = size;
+        if (sm.rpos[d] + size > sm.alloc_lim) {   // would overwrite live events (hybrid kernel): drop
+          sm.ovf = 1;                             // this treat's stores, flag, the run is retried
+          atomicOr(&s.ctl->wheel_overflow, 4u);
+        }
       }
       sm.hbase[d] = sm.rpos[d] + sm.rfill[d];
       sm.rfill[d] += cnt;
@@ -225,10 +231,12 @@ __device__ void flush_sorted(const Dev& s, Smem& sm, long long t, unsigned regio
     }
   }
   __syncthreads();
-  for (unsigned i = threadIdx.x; i < n; i += THREADS) {
-    const unsigned long long e = sm.qp[i];
-    const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
-    st_hint(s.ev + ((sm.hbase[d] + sm.rank[i]) & s.ev_mask), e & ((1ull << EV_DELAY_SHIFT) - 1), pol_first());
+  if (!sm.ovf) {
+    for (unsigned i = threadIdx.x; i < n; i += THREADS) {
+      const unsigned long long e = sm.qp[i];
+      const unsigned d = (unsigned)(e >> EV_DELAY_SHIFT);
+      st_hint(s.ev + ((sm.hbase[d] + sm.rank[i]) & s.ev_mask), e & ((1ull << EV_DELAY_SHIFT) - 1), pol_first());
+    }
   }
   __syncthreads();
 }
@@ -278,7 +286,7 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
 
 // Start-of-cycle bookkeeping (block 0, thread 0, before the fire phase).
 __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
-  reset_acc(&s.ctl->acc[(v.c + 1) % 3]);
+  reset_acc(&s.ctl->acc[(v.c + 1) % NACC]);
   s.ctl->ts0 = globaltimer_ns();
   // staircase: target arrivals are resolved per cycle; the list of the previous cycle's parity (read by
   // its decide, which this thread ran) is emptied for the next cycle — the fires of THIS cycle, which
@@ -298,7 +306,7 @@ __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
 // chunk counts over the block's runs lives in shared memory).
 template <int D, bool PEER = false, int FI = FIRE_ITEMS>   // FI: events per lane per chunk
 __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
-  Acc* acc = &s.ctl->acc[v.c % 3];
+  Acc* acc = &s.ctl->acc[v.c % NACC];
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
   const unsigned vb = blockIdx.x - s.blk0;
   if (threadIdx.x == 0) s.bndesc[(size_t)((v.t - v.delta) & (WHEEL - 1)) * s.nblocks + vb] = 0;
@@ -506,7 +514,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
 // event allocated by a cycle c' with t(c') + f1max > t was still live and the
 // treat's allocations must not have reached it).  *need = ring slots needed.
 __device__ Prop wheel_propose(const Dev& s, const View& v, long long* need) {
-  Acc* a = &s.ctl->acc[v.c % 3];
+  Acc* a = &s.ctl->acc[v.c % NACC];
   Ctl* C = s.ctl;
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
   const long long pl = __ldcg((const long long*)&a->pend_lanes);
@@ -541,7 +549,7 @@ __device__ Prop wheel_propose(const Dev& s, const View& v, long long* need) {
 // 32 slots per step instead of one dependent load after another.
 __device__ Prop wheel_propose_warp(const Dev& s, const View& v, long long* need) {
   const unsigned lane = threadIdx.x & 31u;
-  Acc* a = &s.ctl->acc[v.c % 3];
+  Acc* a = &s.ctl->acc[v.c % NACC];
   Ctl* C = s.ctl;
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
   Prop p;
@@ -589,7 +597,7 @@ __device__ Prop wheel_propose_warp(const Dev& s, const View& v, long long* need)
 // only state no block writes during decide.
 __device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gext = nullptr,
                              const Prop* lpre = nullptr, long long need_pre = 0) {
-  Acc* a = &s.ctl->acc[v.c % 3];
+  Acc* a = &s.ctl->acc[v.c % NACC];
   Ctl* C = s.ctl;
   View nv = v;
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
@@ -676,8 +684,8 @@ __device__ void wheel_decide(const Dev& s, View& v, bool writer, const Prop* gex
     nv.lmode = !s.slab && __ldcg(&a->triggered) <= s.list_max;
     if (writer) {
       if (npl + npp > C->peak_phantoms) C->peak_phantoms = npl + npp;
-      C->acc[(v.c + 1) % 3].pend_lanes = npl;
-      C->acc[(v.c + 1) % 3].pend_phantoms = npp;
+      C->acc[(v.c + 1) % NACC].pend_lanes = npl;
+      C->acc[(v.c + 1) % NACC].pend_phantoms = npp;
     }
   }
   if (writer) C->view = nv;
@@ -718,7 +726,7 @@ __global__ void k_slab_reduce(Ctl* const* ctls, int nslabs) {
 __global__ void __launch_bounds__(THREADS) k_slab_apply(Dev s, const unsigned long long* in, unsigned dst0) {
   const View v = s.ctl->view;
   if (v.status != ST_RUNNING || v.c == 0) return;
-  Acc* acc = &s.ctl->acc[v.c % 3];
+  Acc* acc = &s.ctl->acc[v.c % NACC];
   for (unsigned i = blockIdx.x * THREADS + threadIdx.x; i < s.plane; i += gridDim.x * THREADS) {
     const unsigned long long w = __ldcg(in + i);
     if ((unsigned)(w >> 48) != v.stamp) continue;
@@ -785,7 +793,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_persistent(Dev s) {
       if (!grid_sync(s.ctl, target, sm, s.trace_cap > 0 ? &s.ctl->fin[v.c & 1][0][0] : nullptr)) return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
-    if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % 3].bhit);
+    if (threadIdx.x == 0) sm.bhit = __ldcg(&s.ctl->acc[v.c % NACC].bhit);
     __syncthreads();
     const unsigned long long bhit = sm.bhit;
     __syncthreads();
@@ -835,7 +843,7 @@ __global__ void __launch_bounds__(THREADS, WCSP_MINB) k_wheel_treat(Dev s) {
   load_view(s, sm, v);
   if (v.status != ST_RUNNING) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
-  if (__ldcg(&s.ctl->acc[v.c % 3].bhit) && !s.staircase) return;
+  if (__ldcg(&s.ctl->acc[v.c % NACC].bhit) && !s.staircase) return;
   phase_treat<D, true>(s, v, sm);
 }
 
@@ -851,6 +859,213 @@ __global__ void k_wheel_decide(Dev s) {
 __global__ void __launch_bounds__(THREADS) k_wheel_maintain(Dev s) {
   const long long t = ((volatile View*)&s.ctl->view)->t;
   wheel_maintain(s, t);
+}
+
+// ---------------------------------------------------------------------------
+// One-barrier hybrid kernel (single device, dense wheel cycles).  The two-barrier kernel meets the
+// whole grid after every fire and after every treat.  Here a block starts fire(c+1) as soon as the
+// blocks within hyb_R of it have finished treat(c) — the only blocks whose treat reads or clears
+// state words, temporary labels or bitmap words its fire writes (neighbours are at most one stride
+// of the last axis away, so block distances are bounded) — and only the barrier after the fire,
+// which every decision needs (a target reached, nothing live, an overflow), stays global.  The
+// decision for cycle c is taken after that barrier from fire(c) and treat(c - 1); time advances by 1
+// whenever fire(c) delivered anything (treat(c) may start edges with f1 = 1) and otherwise jumps to
+// the next bucket the finished treats filled, and a cycle is counted only if it fired something,
+// so outputs AND every work counter equal the two-barrier kernel's (tier 5's).  Sparse (listed)
+// cycles treat vertices anywhere, so they end with a grid barrier as before.  Requires f1max < 128
+// (the bucket of cycle c - 2 is recycled while far blocks may still be filing cycle-(c - 1) events).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void wheel_cycle_start_hyb(const Dev& s, const View& v) {
+  reset_acc(&s.ctl->acc[(v.c + 1) % NACC]);
+  s.ctl->ts0 = globaltimer_ns();
+  unsigned long long* nf = &s.ctl->fin[(v.c + 1) & 1][0][0];
+  nf[0] = 0; nf[1] = 0; nf[2] = 0; nf[3] = 0;
+  if (v.c >= 2) {                  // bucket of cycle c - 2: every decision that read its count is done
+    const unsigned b2 = (unsigned)(__ldcg((const long long*)&s.ctl->hist_t[(v.c - 2) & (WHEEL - 1)]) & (WHEEL - 1));
+    s.bnev[b2] = 0; s.bnlane[b2] = 0;
+  }
+  s.ctl->hist_t[v.c & (WHEEL - 1)] = v.t;
+  s.ctl->hist_head[v.c & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
+}
+
+// Neighbourhood wait (thread 0): every block within hyb_R has published prog >= c.
+__device__ __forceinline__ bool local_wait(const Dev& s, Smem& sm, unsigned long long c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int b = (int)blockIdx.x, G = (int)gridDim.x;
+    const int lo = max(0, b - s.hyb_R), hi = min(G - 1, b + s.hyb_R);
+    const unsigned long long t0 = globaltimer_ns();
+    unsigned ok = 1;
+    for (int j = lo; j <= hi && ok; ++j) {
+      while (ld_acquire(s.prog + j) < c) {
+        __nanosleep(32);
+        if (*(volatile unsigned*)&s.ctl->abort) { ok = 0; break; }
+        if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&s.ctl->abort, 1u); ok = 0; break; }
+      }
+    }
+    __threadfence();
+    sm.flag = ok;
+  }
+  __syncthreads();
+  const bool ok = sm.flag != 0;
+  __syncthreads();
+  return ok;
+}
+
+__device__ __forceinline__ void publish_treat(const Dev& s, unsigned long long done) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release_gpu(s.prog + blockIdx.x, done);
+  }
+}
+
+// The decision after fire(c) (warp 0 of every block; lane 0 of block 0 writes the totals).  Returns
+// the view of cycle c + 1 or a terminal status; *lim = ring positions treat(c) may allocate below.
+__device__ View decide_hyb(const Dev& s, const View& v, bool writer, unsigned long long* lim) {
+  const unsigned lane = threadIdx.x & 31u;
+  Ctl* C = s.ctl;
+  Acc* a = &C->acc[v.c % NACC];                        // fire(c); pend at the top of cycle c-1 in ap
+  Acc* ap = &C->acc[(v.c + NACC - 1) % NACC];          // treat(c - 1)
+  const unsigned b = (unsigned)(v.t & (WHEEL - 1));
+  const long long fired = v.c > 0 ? (long long)__ldcg(s.bnev + b) : 0;
+  const long long fired_l = v.c > 0 ? (long long)__ldcg(s.bnlane + b) : 0;
+  long long pl = 0, pp = 0;                            // events in flight at the top of cycle c
+  if (v.c > 0) {
+    const unsigned bp = (unsigned)(__ldcg((const long long*)&C->hist_t[(v.c - 1) & (WHEEL - 1)]) & (WHEEL - 1));
+    const long long fp = v.c > 1 ? (long long)__ldcg(s.bnev + bp) : 0;
+    const long long fpl = v.c > 1 ? (long long)__ldcg(s.bnlane + bp) : 0;
+    pl = __ldcg((const long long*)&ap->pend_lanes) - fpl + (long long)__ldcg(&ap->started);
+    pp = __ldcg((const long long*)&ap->pend_phantoms) - (fp - fpl) + (long long)__ldcg(&ap->created);
+  }
+  const bool counted = v.c > 0 && (s.unit || fired > 0);
+  const unsigned long long bhit = v.c > 0 ? __ldcg(&a->bhit) : 0ull;
+  // ring: the oldest cycle whose events may still be live after t(c) (as wheel_propose_warp)
+  const unsigned long long head = __ldcg(&C->ev_head);
+  const unsigned limc = min((unsigned)WHEEL, v.c + 1u);
+  unsigned B = limc;
+  for (unsigned b0 = 0; b0 < limc; b0 += 32) {
+    const unsigned back = b0 + lane;
+    const bool done = back < limc && __ldcg((const long long*)&C->hist_t[(v.c - back) & (WHEEL - 1)]) + s.f1max <= v.t;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, done);
+    if (m) { B = b0 + (unsigned)(__ffs(m) - 1); break; }
+  }
+  const unsigned long long oldest = B == 0 ? head : __ldcg(&C->hist_head[(v.c - (B - 1)) & (WHEEL - 1)]);
+  *lim = oldest + s.ev_mask + 1;
+  const bool ovf = __ldcg(&C->wheel_overflow) != 0 || head - oldest > s.ev_mask + 1;
+  // next time: + 1 after a fire that delivered something (treat(c) may file delay-1 events) or at
+  // c = 0 (the treatment of A); otherwise the next bucket the finished treats filled
+  unsigned k = 1;
+  if (!s.unit && v.c > 0 && fired == 0) {
+    k = WHEEL;
+    for (unsigned k0 = 1; k0 < (unsigned)WHEEL; k0 += 32) {
+      const unsigned kk = k0 + lane;
+      const bool nz = kk < (unsigned)WHEEL && __ldcg(s.bnev + ((b + kk) & (WHEEL - 1))) != 0;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, nz);
+      if (m) { k = k0 + (unsigned)(__ffs(m) - 1); break; }
+    }
+  }
+  View nv = v;
+  if (lane == 0) {
+    if (writer) {
+      // trace: the record of a counted cycle gets its fire half now and its treat half (triggered,
+      // created, relabels, tested) at the next decision, which is when treat(c - 1) is complete
+      if (v.pad_ && v.ncount > 0 && (long long)v.ncount - 1 < s.trace_cap) {
+        TraceRec& r = s.trace[v.ncount - 1];
+        r.triggered = (long long)__ldcg(&ap->triggered);
+        r.created = (long long)__ldcg(&ap->created);
+        r.relabels = (long long)__ldcg(&ap->relabels);
+        r.tested = (long long)__ldcg(&ap->tested);
+      }
+      if (counted) {
+        C->cycles += 1;
+        C->edge_updates += pl + pp;
+        if ((long long)v.ncount < s.trace_cap) {
+          TraceRec r{v.t, (long long)v.delta, 0, pl, pp, 0, (long long)__ldcg(&a->arrivals), 0, 0, 0, 0, 0, 0, 0};
+          s.trace[v.ncount] = r;
+        }
+      }
+      C->arrivals += __ldcg(&a->arrivals);
+      C->triggered += __ldcg(&ap->triggered); C->created += __ldcg(&ap->created);
+      C->relabels += __ldcg(&ap->relabels); C->started += __ldcg(&ap->started);
+      if (pl + pp > C->peak_phantoms) C->peak_phantoms = pl + pp;
+      a->pend_lanes = pl;              // read as "pend at the top of cycle c" by the next decision
+      a->pend_phantoms = pp;
+    }
+    nv.ncount = v.ncount + (counted ? 1u : 0u);
+    nv.pad_ = counted ? 1u : 0u;      // "the previous cycle was counted" for the next decision
+    if (bhit) {
+      nv.status = 0;                   // 1°: the terminating cycle skips the treat (reading R-new-3)
+      if (writer) resolve_hit(s, bhit, v.t, v.c);
+    } else if (ovf) {
+      nv.status = 8;
+      if (writer) C->need_pool = __ldcg(&C->wheel_overflow) & 2u ? -2 : (long long)(head - oldest) + 1;
+    } else if (v.c > 0 && pl + pp == 0) {
+      nv.status = 1;                   // 2°: nothing was in flight at the top of cycle c
+    } else if (s.budget > 0 && (long long)nv.ncount >= s.budget) {
+      nv.status = 4;
+    } else {
+      nv.delta = k;
+      nv.t = v.t + k;
+      nv.c = v.c + 1;
+      nv.stamp = stamp_of(nv.c);
+      const unsigned long long per = (unsigned long long)(__ldcg(&ap->started) + __ldcg(&ap->created)) * 2ull /
+                                     ((unsigned long long)s.nblocks * (unsigned long long)max(1, s.f1max));
+      unsigned r = 128;
+      while (r < per && r < 4096u) r <<= 1;
+      nv.region = v.c > 0 ? r : v.region;
+      nv.lmode = __ldcg(&ap->triggered) <= s.list_max && v.c > 0;
+    }
+    if (writer) C->view = nv;
+  }
+  return nv;
+}
+
+template <int D, int MINB = WCSP_MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_wheel_hybrid(Dev s) {
+  Smem& sm = smem();
+  init_smem(sm);
+  View v;
+  load_view(s, sm, v);
+  const unsigned long long G = gridDim.x;
+  unsigned long long target = 0;
+  bool glob = true;                // the previous treat ended with a grid barrier (or there was none)
+  while (v.status == ST_RUNNING) {
+    if (v.c > 0) {
+      if (!glob && !local_wait(s, sm, v.c)) return;   // the neighbourhood finished treat(c - 1)
+      if (blockIdx.x == 0 && threadIdx.x == 0) wheel_cycle_start_hyb(s, v);
+      if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
+      if (MINB < 4 && v.lmode) wheel_fire<D, false, FIRE_ITEMS>(s, v, sm);
+      else wheel_fire<D, false, fire_items<MINB>()>(s, v, sm);
+      target += G;
+      if (!grid_sync(s.ctl, target, sm, s.trace_cap > 0 ? &s.ctl->fin[v.c & 1][0][0] : nullptr)) return;
+    }
+    if (threadIdx.x < 32) {
+      unsigned long long lim = 0;
+      const View nv = decide_hyb(s, v, blockIdx.x == 0, &lim);
+      if (threadIdx.x == 0) { sm.view = nv; sm.alloc_lim = lim; }
+    }
+    __syncthreads();
+    const View nv = sm.view;
+    __syncthreads();
+    if (nv.status != ST_RUNNING) break;
+    if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
+    phase_treat<D, true>(s, v, sm);                     // treat(c) with cycle c's view
+    if (v.lmode || needs_maint(v, nv)) {                // listed vertices lie anywhere / maintenance
+      target += G;
+      if (!grid_sync(s.ctl, target, sm)) return;
+      if (needs_maint(v, nv)) {
+        wheel_maintain(s, nv.t);
+        target += G;
+        if (!grid_sync(s.ctl, target, sm)) return;
+      }
+      glob = true;
+    } else {
+      publish_treat(s, (unsigned long long)v.c + 1);
+      glob = false;
+    }
+    v = nv;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -958,7 +1173,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_peer(const __grid_const
     if (leader && threadIdx.x == 0) s.ctl->ts1 = globaltimer_ns();
     if (threadIdx.x == 0) {          // a target reached in any slab ends the run (1°)
       unsigned long long bh = 0;
-      for (int i = 0; i < s.nslab; ++i) bh = max(bh, __ldcv(&s.pctl[i]->acc[v.c % 3].bhit));
+      for (int i = 0; i < s.nslab; ++i) bh = max(bh, __ldcv(&s.pctl[i]->acc[v.c % NACC].bhit));
       sm.bhit = bh;
     }
     __syncthreads();

@@ -465,6 +465,7 @@ wcsp_status reset_ctl(wcsp_handle* h) {
   c.view.region = 256;
   for (int i = 0; i < NACC; ++i) c.acc[i].dmin = 0xFFFFFFFFu;
   c.acc[0].tl_over = 1;            // cycle 0 treats A from the bitmap (k_init)
+  c.ovf_t = 0x7FFFFFFFFFFFFFFFll;
   CK(cudaMemcpyAsync(h->ctl, h->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
   if (is_wheel(h->eng)) {
     CK(cudaMemsetAsync(h->bcounts, 0, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned), h->stream));
@@ -633,9 +634,13 @@ unsigned long long grown(unsigned long long cap, long long need) {
 // neighbourhood radius in blocks covers twice the largest lane offset (a fire's destinations are one
 // offset from its sources, a treat's neighbour reads one offset from its vertices).  WCSP_HYBRID=0/1.
 bool hybrid_for(wcsp_handle* h) {
+  // default: grids whose vertex state words are more than twice the L2 (the DRAM-resident regime,
+  // where the fire dominates: C5z8 8.64 -> 7.76 s); on C3 / C2, whose state fits L2, the two-barrier
+  // kernel is 0.6 % / 2 % faster (profiles/r02/ab_hybrid.txt)
   const char* e = getenv("WCSP_HYBRID");
-  const bool want = e ? atoi(e) != 0 : HYBRID_DEFAULT;
-  if (!want || h->eng != WCSP_ENGINE_WHEEL || h->slab_index >= 0 || h->staircase || h->f1max >= 128 || !h->prog)
+  const bool want = e ? atoi(e) != 0
+                      : (HYBRID_DEFAULT || (unsigned long long)h->N * sizeof(unsigned long long) > 2ull * (unsigned long long)h->l2_bytes);
+  if (!want || h->eng != WCSP_ENGINE_WHEEL || h->slab_index >= 0 || h->staircase || h->f1max >= 64 || !h->prog)
     return false;
   const Dev s = make_dev(h);
   if (s.ileave || s.wbal) return false;
@@ -645,6 +650,7 @@ bool hybrid_for(wcsp_handle* h) {
   unsigned long long maxoff = 1;
   for (int k = 0; k + 1 < h->d; ++k) maxoff *= (unsigned long long)h->shape[k];
   h->hyb_R = (int)std::min<unsigned long long>((2 * maxoff + span - 1) / span + 1, (unsigned long long)h->grid);
+  if (const char* r = getenv("WCSP_HYB_R")) h->hyb_R = std::max(h->hyb_R, atoi(r));   // A/B: a wider wait
   return true;
 }
 

@@ -158,7 +158,8 @@ struct Ctl {
   unsigned long long fin[2][2][2];    // [cycle & 1][phase][max, sum] block busy times (persistent engines)
   // timing-wheel engine (wcsp_wheel.cuh)
   unsigned long long ev_head;      // logical allocation head of the event ring
-  unsigned wheel_overflow, pad2_;  // 2: descriptor table full
+  unsigned wheel_overflow, pad2_;  // 2: descriptor table full, 4: ring guard (hybrid)
+  long long ovf_t;                 // earliest treat time that flagged an overflow (LLONG_MAX: none)
   long long hist_t[WHEEL];         // time of cycle c (slot c & 255) ...
   unsigned long long hist_head[WHEEL];   // ... and the ring head before its treat
   Prop prop, gprop;                // slab engine: local proposal / reduced proposal
@@ -954,6 +955,9 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 #ifndef WCSP_CLAIM
 #define WCSP_CLAIM 0               // 1: warps claim a round's batches dynamically (measured: C3 +0.6 %, C2 +1.8 %; off)
 #endif
+#ifndef WCSP_NB_L2
+#define WCSP_NB_L2 0               // 1: the Step-4 neighbour words bypass L1 (A/B)
+#endif
 #ifndef WCSP_TREAT_PF
 #define WCSP_TREAT_PF 0            // 1: prefetch the next batch's state word (L2) and weight record (L1)
 #endif
@@ -1075,7 +1079,11 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
       const unsigned u = q + s.off[j];
       swr[j] = test ? (staged(u) ? sm.stg[u - slo] : s.sw[u]) : 0xFFFFull;
 #else
+#if WCSP_NB_L2
+      swr[j] = test ? __ldcg(s.sw + (q + s.off[j])) : 0xFFFFull;   // A/B: neighbour words from L2
+#else
       swr[j] = test ? s.sw[q + s.off[j]] : 0xFFFFull;   // untested lanes read as "removed"
+#endif
 #endif
     }
   }

@@ -63,11 +63,17 @@ template <int MINB> __host__ __device__ constexpr int fire_items() { return MINB
 // also fires the events its slab created, so the atomics of a fire phase
 // walk compact regions of the state array (L2-resident) instead of the
 // whole front at once.
-__device__ __forceinline__ void file_run(const Dev& s, unsigned b, unsigned long long pos, unsigned cnt) {
+// A storage overflow in a treat at time t: the flag for the host, and the earliest such time, which
+// the hybrid kernel's decision reads only once every treat up to that time is complete.
+__device__ __forceinline__ void flag_overflow(const Dev& s, unsigned bit, long long t) {
+  atomicOr(&s.ctl->wheel_overflow, bit);
+  atomicMin(&s.ctl->ovf_t, t);
+}
+__device__ __forceinline__ void file_run(const Dev& s, unsigned b, unsigned long long pos, unsigned cnt, long long t) {
   const size_t slot = (size_t)b * s.nblocks + (blockIdx.x - s.blk0);
   const unsigned k = atomicAdd(s.bndesc + slot, 1u);
   if (k < s.dcap) s.bdesc[slot * s.dcap + k] = (pos << 24) | cnt;
-  else atomicOr(&s.ctl->wheel_overflow, 2u);
+  else flag_overflow(s, 2u, t);
 }
 
 __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long long rec, unsigned delay, long long t) {
@@ -91,12 +97,12 @@ __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long lon
     s.spill[(size_t)(blockIdx.x - s.blk0) * s.spill_cap + ks] = rec | ((unsigned long long)delay << EV_DELAY_SHIFT);
   } else {                          // ... else file the event as a run of one (rare)
     const unsigned long long pos = atomicAdd(&s.ctl->ev_head, 1ull);
-    if (pos + 1 > sm.alloc_lim) { sm.ovf = 1; atomicOr(&s.ctl->wheel_overflow, 4u); return; }
+    if (pos + 1 > sm.alloc_lim) { sm.ovf = 1; flag_overflow(s, 4u, t); return; }
     s.ev[pos & s.ev_mask] = rec;
     const unsigned b = (unsigned)((t + delay) & (WHEEL - 1));
     atomicAdd(s.bnev + b, 1u);
     if ((rec >> EV_LANE_BIT) & 1) atomicAdd(s.bnlane + b, 1u);
-    file_run(s, b, pos, 1u);
+    file_run(s, b, pos, 1u, t);
   }
 }
 
@@ -142,7 +148,7 @@ __device__ void warp_flush(const Dev& s, Smem& sm, long long t, unsigned region)
     volatile unsigned* rcap = sm.rcap;
     volatile unsigned long long* rpos = sm.rpos;
     if (rfill[d] + cnt > rcap[d]) {
-      if (rfill[d]) file_run(s, b, rpos[d], rfill[d]);
+      if (rfill[d]) file_run(s, b, rpos[d], rfill[d], t);
       const unsigned size = max(region, cnt);
       rpos[d] = atomicAdd(&s.ctl->ev_head, (unsigned long long)size);
       rfill[d] = 0;
@@ -188,7 +194,7 @@ __device__ void ev_push_warp(const Dev& s, Smem& sm, bool pred, unsigned long lo
 __device__ void regions_close(const Dev& s, Smem& sm, long long t) {
   __syncthreads();
   for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
-    if (sm.rfill[d]) file_run(s, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d]);
+    if (sm.rfill[d]) file_run(s, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d], t);
     sm.rfill[d] = 0;
     sm.rcap[d] = 0;
   }
@@ -214,14 +220,14 @@ __device__ void flush_sorted(const Dev& s, Smem& sm, long long t, unsigned regio
     if (cnt) {
       const unsigned b = (unsigned)((t + d) & (WHEEL - 1));
       if (sm.rfill[d] + cnt > sm.rcap[d]) {
-        if (sm.rfill[d]) file_run(s, b, sm.rpos[d], sm.rfill[d]);
+        if (sm.rfill[d]) file_run(s, b, sm.rpos[d], sm.rfill[d], t);
         const unsigned size = max(region, cnt);
         sm.rpos[d] = atomicAdd(&s.ctl->ev_head, (unsigned long long)size);
         sm.rfill[d] = 0;
         sm.rcap[d] = size;
         if (sm.rpos[d] + size > sm.alloc_lim) {   // would overwrite live events (hybrid kernel): drop
           sm.ovf = 1;                             // this treat's stores, flag, the run is retried
-          atomicOr(&s.ctl->wheel_overflow, 4u);
+          flag_overflow(s, 4u, t);
         }
       }
       sm.hbase[d] = sm.rpos[d] + sm.rfill[d];
@@ -276,7 +282,7 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
   if (threadIdx.x == 0) { sm.np = 0; sm.nspill = 0; }
   if (final_flush) {
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
-      if (sm.rfill[d]) file_run(s, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d]);
+      if (sm.rfill[d]) file_run(s, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d], t);
       sm.rfill[d] = 0;
       sm.rcap[d] = 0;
     }
@@ -872,17 +878,19 @@ __global__ void __launch_bounds__(THREADS) k_wheel_maintain(Dev s) {
 // whenever fire(c) delivered anything (treat(c) may start edges with f1 = 1) and otherwise jumps to
 // the next bucket the finished treats filled, and a cycle is counted only if it fired something,
 // so outputs AND every work counter equal the two-barrier kernel's (tier 5's).  Sparse (listed)
-// cycles treat vertices anywhere, so they end with a grid barrier as before.  Requires f1max < 128
-// (the bucket of cycle c - 2 is recycled while far blocks may still be filing cycle-(c - 1) events).
+// cycles treat vertices anywhere, so they end with a grid barrier as before.  Requires f1max < 64
+// (the bucket of cycle c - 3 is recycled while far blocks may still be filing events of cycles c - 1, c).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void wheel_cycle_start_hyb(const Dev& s, const View& v) {
   reset_acc(&s.ctl->acc[(v.c + 1) % NACC]);
   s.ctl->ts0 = globaltimer_ns();
   unsigned long long* nf = &s.ctl->fin[(v.c + 1) & 1][0][0];
   nf[0] = 0; nf[1] = 0; nf[2] = 0; nf[3] = 0;
-  if (v.c >= 2) {                  // bucket of cycle c - 2: every decision that read its count is done
-    const unsigned b2 = (unsigned)(__ldcg((const long long*)&s.ctl->hist_t[(v.c - 2) & (WHEEL - 1)]) & (WHEEL - 1));
-    s.bnev[b2] = 0; s.bnlane[b2] = 0;
+  if (v.c >= 3) {                  // bucket of cycle c - 3: the last decision that read its count (that
+                                   // of cycle c - 2) ended before the barrier of cycle c - 1 that this
+                                   // block has passed; with f1max < 64 no treat still running files into it
+    const unsigned b3 = (unsigned)(__ldcg((const long long*)&s.ctl->hist_t[(v.c - 3) & (WHEEL - 1)]) & (WHEEL - 1));
+    s.bnev[b3] = 0; s.bnlane[b3] = 0;
   }
   s.ctl->hist_t[v.c & (WHEEL - 1)] = v.t;
   s.ctl->hist_head[v.c & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
@@ -952,7 +960,9 @@ __device__ View decide_hyb(const Dev& s, const View& v, bool writer, unsigned lo
   }
   const unsigned long long oldest = B == 0 ? head : __ldcg(&C->hist_head[(v.c - (B - 1)) & (WHEEL - 1)]);
   *lim = oldest + s.ev_mask + 1;
-  const bool ovf = __ldcg(&C->wheel_overflow) != 0 || head - oldest > s.ev_mask + 1;
+  // an overflow of treat(c - 1) or earlier (every decision input is frozen by the barrier after fire(c):
+  // a treat(c) already running elsewhere may flag its own overflow, which the next decision sees)
+  const bool ovf = v.c > 0 && __ldcg((const long long*)&C->ovf_t) < v.t;
   // next time: + 1 after a fire that delivered something (treat(c) may file delay-1 events) or at
   // c = 0 (the treatment of A); otherwise the next bucket the finished treats filled
   unsigned k = 1;
@@ -1000,6 +1010,7 @@ __device__ View decide_hyb(const Dev& s, const View& v, bool writer, unsigned lo
     } else if (ovf) {
       nv.status = 8;
       if (writer) C->need_pool = __ldcg(&C->wheel_overflow) & 2u ? -2 : (long long)(head - oldest) + 1;
+      (void)head;
     } else if (v.c > 0 && pl + pp == 0) {
       nv.status = 1;                   // 2°: nothing was in flight at the top of cycle c
     } else if (s.budget > 0 && (long long)nv.ncount >= s.budget) {
@@ -1030,6 +1041,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_hybrid(Dev s) {
   const unsigned long long G = gridDim.x;
   unsigned long long target = 0;
   bool glob = true;                // the previous treat ended with a grid barrier (or there was none)
+  long long t_list = -(1ll << 40); // time of the last listed (sparse) treat: its vertices lay anywhere,
+                                   // so the events it filed fire from blocks far from their sources
+                                   // until t_list + f1max — those fires need the grid barrier too
   while (v.status == ST_RUNNING) {
     if (v.c > 0) {
       if (!glob && !local_wait(s, sm, v.c)) return;   // the neighbourhood finished treat(c - 1)
@@ -1051,7 +1065,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_hybrid(Dev s) {
     if (nv.status != ST_RUNNING) break;
     if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
     phase_treat<D, true>(s, v, sm);                     // treat(c) with cycle c's view
-    if (v.lmode || needs_maint(v, nv)) {                // listed vertices lie anywhere / maintenance
+    if (v.lmode) t_list = v.t;
+    if (v.lmode || needs_maint(v, nv) || nv.t <= t_list + s.f1max) {   // listed vertices / their events / maint
       target += G;
       if (!grid_sync(s.ctl, target, sm)) return;
       if (needs_maint(v, nv)) {

@@ -547,3 +547,38 @@ def test_both_cycle_kernel_builds(bps, monkeypatch):
         for slabs in (2, 4):         # the fused peer-halo kernel comes in the same two builds
             rp = wcsp.solve(I.config_face(shape, seed, M), engine="wheel", slabs=slabs, halo="peer")
             assert rp.key() == r.key() and model_counters(rp) == model_counters(r), (shape, slabs, rp, r)
+
+
+@pytest.mark.parametrize("hyb", ["1"])
+def test_hybrid_one_barrier_kernel(hyb, monkeypatch):
+    """The one-barrier hybrid kernel (k_wheel_hybrid; WCSP_HYBRID=1 forces it on every
+    single-device persistent wheel solve): neighbourhood waits replace the grid barrier after
+    the treat, time advances by 1 after a fire that delivered water and jumps otherwise, and
+    only non-empty cycles are counted — outputs equal the oracle's and every work counter
+    tier 5's, on random grids (holes, several sources/targets, M = infinity), sparse-cycle
+    runs (the fractal, listed treats), repeated solves (no run-to-run difference), a tiny
+    event ring (the allocation guard and the regrow) and both kernel builds."""
+    monkeypatch.setenv("WCSP_HYBRID", hyb)
+    rng = np.random.default_rng(4321)
+    for i in range(80):
+        inst = I.random_small(rng, shapes=[(12, 12), (6, 6, 6), (30, 9), (3, 4, 3, 3), (40,), (16, 16, 16)],
+                              M_range=(5, 120), max_sources=4, max_targets=4, hole_prob=0.1 if i % 3 == 0 else 0.0)
+        if i % 7 == 3:
+            inst = inst.with_M(I.M_INF)
+        check(inst, "wheel")
+    for k in (5, 8):
+        f = I.fractal_instance(k)
+        check(f, "wheel")
+        check(f.with_M((1 << k) + 1), "wheel")
+    for inst in (I.config_face((48, 48, 48), 0, 260), I.config_face((200, 200), 6, 700)):
+        m, mc = oracle.solve_model(inst)
+        want = (mc.cycles, mc.work, mc.arrivals, mc.triggered, mc.created, mc.started, mc.relabels)
+        with wcsp.Solver(inst, engine="wheel") as s:
+            for _ in range(4):
+                r = s.solve()
+                assert r.key() == m.key() and model_counters(r) == want, (inst.name, r)
+        r = wcsp.solve(inst, engine="wheel", phantom_capacity=4096)
+        assert r.retries >= 1 and r.key() == m.key() and model_counters(r) == want, r
+    for bps in ("3", "4"):
+        monkeypatch.setenv("WCSP_BLOCKS_PER_SM", bps)
+        check(I.config_face((64, 48, 32), 2, 260), "wheel")

@@ -623,7 +623,7 @@ wcsp_status solve_once(wcsp_handle* h, wcsp_result* r, int* status) {
 // (2x once the structure is past 2^26 entries, where memory matters).
 constexpr int MAX_ATTEMPTS = 12;
 #ifndef HYBRID_DEFAULT
-#define HYBRID_DEFAULT false
+#define HYBRID_DEFAULT true
 #endif
 unsigned long long grown(unsigned long long cap, long long need) {
   const unsigned long long f = cap < (1ull << 26) ? 4 : 2;
@@ -634,12 +634,10 @@ unsigned long long grown(unsigned long long cap, long long need) {
 // neighbourhood radius in blocks covers twice the largest lane offset (a fire's destinations are one
 // offset from its sources, a treat's neighbour reads one offset from its vertices).  WCSP_HYBRID=0/1.
 bool hybrid_for(wcsp_handle* h) {
-  // default: grids whose vertex state words are more than twice the L2 (the DRAM-resident regime,
-  // where the fire dominates: C5z8 8.64 -> 7.76 s); on C3 / C2, whose state fits L2, the two-barrier
-  // kernel is 0.6 % / 2 % faster (profiles/r02/ab_hybrid.txt)
+  // default on (profiles/r02/ab_hybrid.txt, warp-parallel neighbourhood wait): C3 132.8 -> 131.0 ms,
+  // C2 99.6 -> 95.2 ms, C5z8 8.62 -> 7.74 s; C3s 14.65 -> 15.29 ms is the one measured loss
   const char* e = getenv("WCSP_HYBRID");
-  const bool want = e ? atoi(e) != 0
-                      : (HYBRID_DEFAULT || (unsigned long long)h->N * sizeof(unsigned long long) > 2ull * (unsigned long long)h->l2_bytes);
+  const bool want = e ? atoi(e) != 0 : HYBRID_DEFAULT;
   if (!want || h->eng != WCSP_ENGINE_WHEEL || h->slab_index >= 0 || h->staircase || h->f1max >= 64 || !h->prog)
     return false;
   const Dev s = make_dev(h);

@@ -69,7 +69,11 @@ __device__ __forceinline__ void flag_overflow(const Dev& s, unsigned bit, long l
   atomicOr(&s.ctl->wheel_overflow, bit);
   atomicMin(&s.ctl->ovf_t, t);
 }
-__device__ __forceinline__ void file_run(const Dev& s, unsigned b, unsigned long long pos, unsigned cnt, long long t) {
+__device__ __forceinline__ void file_run(const Dev& s, const Smem& sm, unsigned b, unsigned long long pos, unsigned cnt,
+                                         long long t) {
+  // after the ring guard fired in this block (hybrid kernel) nothing more is filed: the run is void
+  // and is retried, but a neighbour's or this block's next fire must not read unwritten slots
+  if (sm.ovf) return;
   const size_t slot = (size_t)b * s.nblocks + (blockIdx.x - s.blk0);
   const unsigned k = atomicAdd(s.bndesc + slot, 1u);
   if (k < s.dcap) s.bdesc[slot * s.dcap + k] = (pos << 24) | cnt;
@@ -102,7 +106,7 @@ __device__ void ev_stage(const Dev& s, Smem& sm, unsigned idx, unsigned long lon
     const unsigned b = (unsigned)((t + delay) & (WHEEL - 1));
     atomicAdd(s.bnev + b, 1u);
     if ((rec >> EV_LANE_BIT) & 1) atomicAdd(s.bnlane + b, 1u);
-    file_run(s, b, pos, 1u, t);
+    file_run(s, sm, b, pos, 1u, t);
   }
 }
 
@@ -148,7 +152,7 @@ __device__ void warp_flush(const Dev& s, Smem& sm, long long t, unsigned region)
     volatile unsigned* rcap = sm.rcap;
     volatile unsigned long long* rpos = sm.rpos;
     if (rfill[d] + cnt > rcap[d]) {
-      if (rfill[d]) file_run(s, b, rpos[d], rfill[d], t);
+      if (rfill[d]) file_run(s, sm, b, rpos[d], rfill[d], t);
       const unsigned size = max(region, cnt);
       rpos[d] = atomicAdd(&s.ctl->ev_head, (unsigned long long)size);
       rfill[d] = 0;
@@ -194,7 +198,7 @@ __device__ void ev_push_warp(const Dev& s, Smem& sm, bool pred, unsigned long lo
 __device__ void regions_close(const Dev& s, Smem& sm, long long t) {
   __syncthreads();
   for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
-    if (sm.rfill[d]) file_run(s, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d], t);
+    if (sm.rfill[d]) file_run(s, sm, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d], t);
     sm.rfill[d] = 0;
     sm.rcap[d] = 0;
   }
@@ -220,7 +224,7 @@ __device__ void flush_sorted(const Dev& s, Smem& sm, long long t, unsigned regio
     if (cnt) {
       const unsigned b = (unsigned)((t + d) & (WHEEL - 1));
       if (sm.rfill[d] + cnt > sm.rcap[d]) {
-        if (sm.rfill[d]) file_run(s, b, sm.rpos[d], sm.rfill[d], t);
+        if (sm.rfill[d]) file_run(s, sm, b, sm.rpos[d], sm.rfill[d], t);
         const unsigned size = max(region, cnt);
         sm.rpos[d] = atomicAdd(&s.ctl->ev_head, (unsigned long long)size);
         sm.rfill[d] = 0;
@@ -282,7 +286,7 @@ __device__ void ev_flush(const Dev& s, Smem& sm, long long t, unsigned region, b
   if (threadIdx.x == 0) { sm.np = 0; sm.nspill = 0; }
   if (final_flush) {
     for (unsigned d = threadIdx.x; d < WHEEL; d += THREADS) {
-      if (sm.rfill[d]) file_run(s, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d], t);
+      if (sm.rfill[d]) file_run(s, sm, (unsigned)((t + d) & (WHEEL - 1)), sm.rpos[d], sm.rfill[d], t);
       sm.rfill[d] = 0;
       sm.rcap[d] = 0;
     }
@@ -896,23 +900,33 @@ __device__ __forceinline__ void wheel_cycle_start_hyb(const Dev& s, const View& 
   s.ctl->hist_head[v.c & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
 }
 
-// Neighbourhood wait (thread 0): every block within hyb_R has published prog >= c.
+// Neighbourhood wait (warp 0, one progress word per lane, polled together): every block within
+// hyb_R has published prog >= c.
 __device__ __forceinline__ bool local_wait(const Dev& s, Smem& sm, unsigned long long c) {
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
     const int b = (int)blockIdx.x, G = (int)gridDim.x;
     const int lo = max(0, b - s.hyb_R), hi = min(G - 1, b + s.hyb_R);
     const unsigned long long t0 = globaltimer_ns();
     unsigned ok = 1;
-    for (int j = lo; j <= hi && ok; ++j) {
-      while (ld_acquire(s.prog + j) < c) {
+    for (int j0 = lo; j0 <= hi; j0 += 32) {
+      const int j = j0 + (int)lane;
+      for (;;) {
+        const bool done = j > hi || ld_acquire(s.prog + j) >= c;
+        if (__all_sync(0xFFFFFFFFu, done)) break;
         __nanosleep(32);
-        if (*(volatile unsigned*)&s.ctl->abort) { ok = 0; break; }
-        if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&s.ctl->abort, 1u); ok = 0; break; }
+        unsigned bad = 0;
+        if (lane == 0) {
+          if (*(volatile unsigned*)&s.ctl->abort) bad = 1;
+          else if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&s.ctl->abort, 1u); bad = 1; }
+        }
+        if (__shfl_sync(0xFFFFFFFFu, bad, 0)) { ok = 0; break; }
       }
+      if (!ok) break;
     }
     __threadfence();
-    sm.flag = ok;
+    if (lane == 0) sm.flag = ok;
   }
   __syncthreads();
   const bool ok = sm.flag != 0;

@@ -810,7 +810,9 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
     if (pow2_at_least(ring + slack) <= (1ull << 31)) ring += slack;
     CKH(alloc_ring(h, opt.phantom_capacity > 0 ? cap : ring));
     const char* dc = getenv("WCSP_DCAP");          // tests: a tiny run-descriptor table forces its overflow path
-    CKH(alloc_desc(h, dc ? (unsigned)std::max(1, atoi(dc)) : 32u));
+    // runs per (bucket, block): one per source cycle and region; big grids file more (C5z8: up to 40
+    // on block 0, which made every fresh handle's first solve overflow 32 and re-run)
+    CKH(alloc_desc(h, dc ? (unsigned)std::max(1, atoi(dc)) : (N >= (1ull << 22) ? 64u : 32u)));
     CKC(cudaMalloc(&h->bcounts, (size_t)WHEEL * (2 + h->grid) * sizeof(unsigned)));
     // spill room per block and flush period: a dense window round (e.g. the initial treatment
     // of a whole boundary) can stage several times the shared-memory staging
@@ -1606,7 +1608,7 @@ extern "C" {
 const char* wcsp_last_error(void) { return g_err.c_str(); }
 
 const char* wcsp_version(void) {
-  return "wcsp-b200 0.3 (sm_100a; engines: sweep/wheel x persistent/stepped; slab partition)";
+  return "wcsp-b200 0.4 (sm_100a; engines: sweep/wheel x persistent/stepped, one-barrier hybrid wheel; wide labels; slab partition)";
 }
 
 wcsp_status wcsp_create(const wcsp_problem* p, const wcsp_options* o, wcsp_handle** out) {

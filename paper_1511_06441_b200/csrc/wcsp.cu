@@ -247,6 +247,7 @@ Dev make_dev(const wcsp_handle* h) {
   s.tlist = h->tlist;
   s.prog = h->prog;
   s.hyb_R = h->hyb_R;
+  s.hyb_prep = getenv("WCSP_HYB_PREP") ? atoi(getenv("WCSP_HYB_PREP")) != 0 : 1;   // A/B switch
   // sparse cycles: about 64 triggered vertices per block (WCSP_LIST_MAX overrides, A/B runs)
   s.list_max = getenv("WCSP_LIST_MAX") ? strtoull(getenv("WCSP_LIST_MAX"), nullptr, 10)
                                        : (unsigned long long)h->grid * 64ull;

@@ -225,6 +225,7 @@ struct Dev {
   // within which blocks' fires and treats touch the same state words
   unsigned long long* prog;        // [nblocks] treats completed (monotone per solve)
   int hyb_R;
+  int hyb_prep;                    // run the fire's own-data prologue before the neighbourhood wait
   // slab partition (multi-GPU / virtual slabs): local index + goff = global index
   unsigned goff;
   unsigned plane;                  // vertices per plane of the partitioned (last) axis
@@ -447,6 +448,7 @@ struct Smem {
   unsigned bm_lo, bm_words;        // wheel fire, dense cycles: the block's triggered bitmap in qp covers
                                    // vertices [bm_lo, bm_lo + 32 * bm_words)
   unsigned base_a, base_b, flag, ovf;
+  unsigned f_nd, f_prep;           // fire: descriptors of this block's bucket; prologue already run
   unsigned long long alloc_lim;    // event-ring allocations of this treat must stay below (hybrid guard)
   View view;
   unsigned long long bhit;
@@ -1538,7 +1540,7 @@ __device__ __forceinline__ void load_view(const Dev& s, Smem& sm, View& v) {
 }
 
 __device__ __forceinline__ void init_smem(Smem& sm) {
-  if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; sm.nspill = 0; sm.ovf = 0; sm.alloc_lim = ~0ull; }
+  if (threadIdx.x == 0) { sm.na = 0; sm.np = 0; sm.nspill = 0; sm.ovf = 0; sm.alloc_lim = ~0ull; sm.f_prep = 0; sm.f_nd = 0; }
 #if WCSP_TREAT_STAGE
   if (threadIdx.x == 0) {
     sm.stg_n = 0; sm.stg_lo = 0; sm.stg_phase = 0;

@@ -314,30 +314,54 @@ __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
 // fires the runs its own slab filed; the runs are cut into chunks of
 // FIRE_ITEMS * 32 events that the block's warps take in turn (a prefix sum of
 // chunk counts over the block's runs lives in shared memory).
-template <int D, bool PEER = false, int FI = FIRE_ITEMS>   // FI: events per lane per chunk
-__device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
-  Acc* acc = &s.ctl->acc[v.c % NACC];
+// run descriptors staged per pass: dpos[MAXD] (u64) + dchunk[MAXD + 1] (u32) in the wl union
+constexpr unsigned FIRE_WL_BYTES = sizeof(Smem::wl);
+constexpr unsigned FIRE_MAXD = ((FIRE_WL_BYTES - 4) / 12 >= 512 ? 512u : ((FIRE_WL_BYTES - 4) / 12) & ~31u);
+static_assert(FIRE_MAXD >= 32 && FIRE_MAXD * 8 + (FIRE_MAXD + 1) * 4 <= FIRE_WL_BYTES,
+              "descriptor staging exceeds Smem::wl");
+
+// One pass of the fire's descriptor staging (warp 0): descriptors [d0, d0 + n) and the prefix sum of
+// their chunk counts, chunks of CH events.
+template <unsigned CH>
+__device__ __forceinline__ void fire_stage(Smem& sm, const unsigned long long* dl, unsigned d0, unsigned n) {
+  unsigned long long* dpos = reinterpret_cast<unsigned long long*>(&sm.wl[0][0]);   // [MAXD]
+  unsigned* dchunk = reinterpret_cast<unsigned*>(dpos + FIRE_MAXD);                   // [MAXD + 1] prefix
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  if (warp != 0) return;
+  unsigned carry = 0;
+  for (unsigned i0 = 0; i0 < n; i0 += 32) {
+    const unsigned i = i0 + lane;
+    unsigned long long dsc = 0;
+    unsigned ch = 0;
+    if (i < n) {
+      dsc = __ldcg(dl + d0 + i);
+      ch = ((unsigned)(dsc & 0xFFFFFFu) + CH - 1) / CH;
+      dpos[i] = dsc;
+    }
+    unsigned x = ch;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if ((int)lane >= o) x += y;
+    }
+    if (i < n) dchunk[i] = carry + x - ch;
+    carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+  }
+  if (lane == 0) dchunk[n] = carry;
+}
+
+// The part of the fire of cycle v that reads only this block's own data: reset of the previous
+// bucket's descriptor count, the block-local bitmap's range and zeroing, and the first pass of the
+// descriptor staging.  The hybrid kernel runs it before its neighbourhood wait (the block's runs for
+// the next bucket are complete once its own treat is), so those dependent loads overlap the wait.
+template <int D, bool PEER = false, int FI = FIRE_ITEMS>
+__device__ void fire_prologue(const Dev& s, const View& v, Smem& sm) {
   const unsigned b = (unsigned)(v.t & (WHEEL - 1));
   const unsigned vb = blockIdx.x - s.blk0;
   if (threadIdx.x == 0) s.bndesc[(size_t)((v.t - v.delta) & (WHEEL - 1)) * s.nblocks + vb] = 0;
   const size_t slot = (size_t)b * s.nblocks + vb;
   const unsigned nd = min(__ldcg(s.bndesc + slot), s.dcap);
-  const unsigned long long* dl = s.bdesc + slot * s.dcap;
-  constexpr unsigned CH = FI * 32;
-  // run descriptors staged per pass: dpos[MAXD] (u64) + dchunk[MAXD + 1] (u32) in the wl union
-  constexpr unsigned WL_BYTES = sizeof(Smem::wl);
-  constexpr unsigned MAXD = ((WL_BYTES - 4) / 12 >= 512 ? 512u : ((WL_BYTES - 4) / 12) & ~31u);
-  static_assert(MAXD >= 32 && MAXD * 8 + (MAXD + 1) * 4 <= WL_BYTES, "descriptor staging exceeds Smem::wl");
-  unsigned long long* dpos = reinterpret_cast<unsigned long long*>(&sm.wl[0][0]);   // [MAXD]
-  unsigned* dchunk = reinterpret_cast<unsigned*>(dpos + MAXD);                        // [MAXD + 1] prefix
-  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  unsigned arr = 0;
-  // Dense cycles: first arrivals near the block's own slab of the grid (its treat windows and one
-  // plane of the last axis on either side: where the events it fires lead) set bits of a
-  // shared-memory bitmap (the treat staging is free during the fire), merged into the global
-  // bitmap with one atomicOr per word at the end; sparse cycles list them (see arrive_post).
   const bool local_bits = (PEER || !s.slab) && !v.lmode;
-  const bool redmode = local_bits;
   if (local_bits) {
     if (threadIdx.x == 0) {
       const unsigned long long ww = s.win_words;
@@ -360,31 +384,42 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
     __syncthreads();
     uint4* bm4 = reinterpret_cast<uint4*>(sm.qp);   // 16-byte stores (qp is 16-byte aligned)
     for (unsigned i = threadIdx.x; i < (sm.bm_words + 3) / 4; i += THREADS) bm4[i] = make_uint4(0u, 0u, 0u, 0u);
+  } else if (threadIdx.x == 0) {
+    sm.bm_lo = 0;
+    sm.bm_words = 0;
   }
+  __syncthreads();
+  if (nd > 0) fire_stage<FI * 32>(sm, s.bdesc + slot * s.dcap, 0, min(FIRE_MAXD, nd));
+  if (threadIdx.x == 0) { sm.f_nd = nd; sm.f_prep = 1; }
+  __syncthreads();
+}
+
+template <int D, bool PEER = false, int FI = FIRE_ITEMS>   // FI: events per lane per chunk
+__device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
+  Acc* acc = &s.ctl->acc[v.c % NACC];
+  const unsigned b = (unsigned)(v.t & (WHEEL - 1));
+  const unsigned vb = blockIdx.x - s.blk0;
+  if (!sm.f_prep) fire_prologue<D, PEER, FI>(s, v, sm);   // not yet run ahead by the hybrid kernel
+  const size_t slot = (size_t)b * s.nblocks + vb;
+  const unsigned nd = sm.f_nd;
+  const unsigned long long* dl = s.bdesc + slot * s.dcap;
+  constexpr unsigned CH = FI * 32;
+  constexpr unsigned MAXD = FIRE_MAXD;
+  unsigned long long* dpos = reinterpret_cast<unsigned long long*>(&sm.wl[0][0]);   // [MAXD]
+  unsigned* dchunk = reinterpret_cast<unsigned*>(dpos + MAXD);                        // [MAXD + 1] prefix
+  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  unsigned arr = 0;
+  // Dense cycles: first arrivals near the block's own slab of the grid (its treat windows and one
+  // plane of the last axis on either side: where the events it fires lead) set bits of a
+  // shared-memory bitmap (the treat staging is free during the fire; set up by fire_prologue),
+  // merged into the global bitmap with one atomicOr per word at the end; sparse cycles list them.
+  const bool local_bits = (PEER || !s.slab) && !v.lmode;
+  const bool redmode = local_bits;
   for (unsigned d0 = 0; d0 < nd; d0 += MAXD) {
     const unsigned n = min(MAXD, nd - d0);
-    __syncthreads();
-    if (warp == 0) {                 // prefix sum of chunk counts (warp 0, MAXD / 32 passes)
-      unsigned carry = 0;
-      for (unsigned i0 = 0; i0 < n; i0 += 32) {
-        const unsigned i = i0 + lane;
-        unsigned long long dsc = 0;
-        unsigned ch = 0;
-        if (i < n) {
-          dsc = __ldcg(dl + d0 + i);
-          ch = ((unsigned)(dsc & 0xFFFFFFu) + CH - 1) / CH;
-          dpos[i] = dsc;
-        }
-        unsigned x = ch;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-          if ((int)lane >= o) x += y;
-        }
-        if (i < n) dchunk[i] = carry + x - ch;
-        carry += __shfl_sync(0xFFFFFFFFu, x, 31);
-      }
-      if (lane == 0) dchunk[n] = carry;
+    if (d0 > 0) {                  // pass 0 was staged by fire_prologue
+      __syncthreads();
+      fire_stage<CH>(sm, dl, d0, n);
     }
     __syncthreads();
     const unsigned nchunks = dchunk[n];
@@ -515,7 +550,7 @@ __device__ void wheel_fire(const Dev& s, const View& v, Smem& sm) {
     }
   }
   block_reduce_commit(sm, 0xFFFFFFFFu, 0, arr, 0, 0, 0, acc);   // (ends with a block barrier:
-  if (threadIdx.x == 0) sm.na = 0;                              //  every thread has read sm.na)
+  if (threadIdx.x == 0) { sm.na = 0; sm.f_prep = 0; }           //  every thread has read sm.na)
 }
 
 // The wheel's local proposal for the decision of cycle c (see Prop): best
@@ -1060,7 +1095,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_hybrid(Dev s) {
                                    // until t_list + f1max — those fires need the grid barrier too
   while (v.status == ST_RUNNING) {
     if (v.c > 0) {
-      if (!glob && !local_wait(s, sm, v.c)) return;   // the neighbourhood finished treat(c - 1)
+      if (!glob) {
+        // the fire's own-data prologue first (descriptor count and staging, bitmap zeroing): its
+        // dependent loads overlap the wait for the neighbourhood to finish treat(c - 1)
+        if (s.hyb_prep) {
+          if (MINB < 4 && v.lmode) fire_prologue<D, false, FIRE_ITEMS>(s, v, sm);
+          else fire_prologue<D, false, fire_items<MINB>()>(s, v, sm);
+        }
+        if (!local_wait(s, sm, v.c)) return;
+      }
       if (blockIdx.x == 0 && threadIdx.x == 0) wheel_cycle_start_hyb(s, v);
       if (threadIdx.x == 0) sm.tphase = globaltimer_ns();
       if (MINB < 4 && v.lmode) wheel_fire<D, false, FIRE_ITEMS>(s, v, sm);

@@ -989,7 +989,7 @@ __device__ View decide_hyb(const Dev& s, const View& v, bool writer, unsigned lo
   const long long fired_l = v.c > 0 ? (long long)__ldcg(s.bnlane + b) : 0;
   long long pl = 0, pp = 0;                            // events in flight at the top of cycle c
   if (v.c > 0) {
-    const unsigned bp = (unsigned)(__ldcg((const long long*)&C->hist_t[(v.c - 1) & (WHEEL - 1)]) & (WHEEL - 1));
+    const unsigned bp = (unsigned)((v.t - v.delta) & (WHEEL - 1));   // the bucket of cycle c - 1
     const long long fp = v.c > 1 ? (long long)__ldcg(s.bnev + bp) : 0;
     const long long fpl = v.c > 1 ? (long long)__ldcg(s.bnlane + bp) : 0;
     pl = __ldcg((const long long*)&ap->pend_lanes) - fpl + (long long)__ldcg(&ap->started);
@@ -1001,13 +1001,26 @@ __device__ View decide_hyb(const Dev& s, const View& v, bool writer, unsigned lo
   const unsigned long long head = __ldcg(&C->ev_head);
   const unsigned limc = min((unsigned)WHEEL, v.c + 1u);
   unsigned B = limc;
+  unsigned long long oldest = head;
   for (unsigned b0 = 0; b0 < limc; b0 += 32) {
+    // each lane loads its cycle's time AND allocation head together, so the head of the oldest live
+    // cycle comes from a shuffle instead of a second dependent load
     const unsigned back = b0 + lane;
-    const bool done = back < limc && __ldcg((const long long*)&C->hist_t[(v.c - back) & (WHEEL - 1)]) + s.f1max <= v.t;
+    const unsigned slot = (v.c - back) & (WHEEL - 1);
+    const long long ht = back < limc ? __ldcg((const long long*)&C->hist_t[slot]) : 0;
+    const unsigned long long hh = back < limc ? __ldcg(&C->hist_head[slot]) : 0ull;
+    const bool done = back < limc && ht + s.f1max <= v.t;
     const unsigned m = __ballot_sync(0xFFFFFFFFu, done);
-    if (m) { B = b0 + (unsigned)(__ffs(m) - 1); break; }
+    const unsigned first = m ? (unsigned)(__ffs(m) - 1) : 32u;          // in this group of 32
+    const unsigned long long hsel = __shfl_sync(0xFFFFFFFFu, hh, first == 0 ? 0 : first - 1);
+    if (m) {
+      B = b0 + first;
+      if (B > 0) oldest = first > 0 ? hsel : oldest;   // first == 0: the last lane of the previous group
+      break;
+    }
+    oldest = __shfl_sync(0xFFFFFFFFu, hh, min(31u, limc - 1u - b0));   // whole group live: its oldest
   }
-  const unsigned long long oldest = B == 0 ? head : __ldcg(&C->hist_head[(v.c - (B - 1)) & (WHEEL - 1)]);
+  if (B == 0) oldest = head;
   *lim = oldest + s.ev_mask + 1;
   // an overflow of treat(c - 1) or earlier (every decision input is frozen by the barrier after fire(c):
   // a treat(c) already running elsewhere may flag its own overflow, which the next decision sees)

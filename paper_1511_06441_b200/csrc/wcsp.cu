@@ -778,6 +778,10 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
                                                     sizeof(Smem)));
   if (per_sm < 1) CKH(fail(WCSP_ECUDA, "cycle kernel cannot be resident"));
   if (bps) per_sm = std::max(1, std::min(per_sm, atoi(bps)));
+  // 2-D grids up to 2^22 vertices: short cycles whose fixed costs (barriers, waits, decisions) grow
+  // with the block count — 2 resident blocks per SM (C2 94.0 -> 89.1 ms, C4 15.9 -> 15.1 ms;
+  // profiles/r02/ab_bps.txt); 3-D grids keep the occupancy their treat gathers need
+  else if (p->d <= 2 && N <= (1ull << 22) && !spec) per_sm = std::min(per_sm, 2);
   if (spec && spec->per_sm > 0) per_sm = spec->per_sm;     // peer-halo slab: sized for the peer kernel
   h->grid = h->grid_main = per_sm * h->nsm;
   h->eng = opt.engine;

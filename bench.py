@@ -443,7 +443,7 @@ def run_ours(args, rank, world, local):
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": {"persistent": "k_persistent<D>", "wheel": "k_wheel_persistent<D>"}.get(
+                "kernel": {"persistent": "k_persistent<D>", "wheel": "k_wheel_hybrid<D,B> (k_wheel_persistent<D> if WCSP_HYBRID=0 or ineligible)"}.get(
                     args.engine, "k_*<D> (stepped: 3 launches per cycle)") + " (cycle kernel)",
                 "alg_bytes_per_launch": ab,
                 "alg_formula": "SURVEY §8(d): 2(E+P) + 13R + (2d*8+22)T + 8C + 2RL over the solve's counters",

@@ -17,6 +17,10 @@
 #include <string>
 #include <vector>
 
+#ifndef HYB_LAG_DEFAULT
+#define HYB_LAG_DEFAULT 1   // lagged-decision wheel kernel where the hybrid applies
+#endif
+
 using namespace wcspk;
 
 namespace {
@@ -159,7 +163,8 @@ cudaError_t set_smem_attrs() {
                  reinterpret_cast<void*>(&k_wheel_peer<D, 3>), reinterpret_cast<void*>(&k_wheel_peer<D, 4>),
                  reinterpret_cast<void*>(&k_persistent<D, true>), reinterpret_cast<void*>(&k_sweep<D, true>),
                  reinterpret_cast<void*>(&k_treat<D, true>), reinterpret_cast<void*>(&k_wheel_hybrid<D, 3>),
-                 reinterpret_cast<void*>(&k_wheel_hybrid<D, 4>)};
+                 reinterpret_cast<void*>(&k_wheel_hybrid<D, 4>), reinterpret_cast<void*>(&k_wheel_lag<D, 3>),
+                 reinterpret_cast<void*>(&k_wheel_lag<D, 4>)};
   const char* co = getenv("WCSP_CARVEOUT");       // A/B runs: shared-memory carveout in percent of L1
   for (void* f : fns) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -492,11 +497,25 @@ void* hybrid_fn(bool big) {
 void* hybrid_fn_d(int d, bool big) {
   return d == 1 ? hybrid_fn<1>(big) : d == 2 ? hybrid_fn<2>(big) : d == 3 ? hybrid_fn<3>(big) : hybrid_fn<4>(big);
 }
+template <int D>
+void* lag_fn(bool big) {
+  return big ? reinterpret_cast<void*>(&k_wheel_lag<D, 4>) : reinterpret_cast<void*>(&k_wheel_lag<D, 3>);
+}
+void* lag_fn_d(int d, bool big) {
+  return d == 1 ? lag_fn<1>(big) : d == 2 ? lag_fn<2>(big) : d == 3 ? lag_fn<3>(big) : lag_fn<4>(big);
+}
+// The lagged-decision kernel (k_wheel_lag) wherever the hybrid applies, unless tracing (its cycle
+// records come from the hybrid's per-cycle decision) or WCSP_HYB_LAG=0 (A/B).
+bool lag_for(const wcsp_handle* h) {
+  const char* e = getenv("WCSP_HYB_LAG");
+  return h->hyb && h->opt.trace_cap == 0 && (e ? atoi(e) != 0 : HYB_LAG_DEFAULT);
+}
 
 wcsp_status run_persistent(wcsp_handle* h) {
   Dev s = make_dev(h);
   void* args[] = {&s};
-  void* fn = h->hyb ? hybrid_fn_d(h->d, h->big) : cycle_fn_d(h->d, h->eng, h->big, h->wide);
+  void* fn = h->hyb ? (lag_for(h) ? lag_fn_d(h->d, h->big) : hybrid_fn_d(h->d, h->big))
+                    : cycle_fn_d(h->d, h->eng, h->big, h->wide);
   CK(cudaLaunchCooperativeKernel(fn, dim3(h->grid), dim3(THREADS), args, sizeof(Smem),
                                  h->stream));
   h->launches += 1;

@@ -113,8 +113,9 @@ struct BArr { unsigned D, cand, src, via; };   // an arrival at a target (termin
 
 // Per-cycle accumulators live in NACC slots (slot c % NACC).  The two-barrier kernels need three
 // (the next cycle's slot is reset while this one is read); the one-barrier hybrid kernel reads a
-// cycle's fire half and the previous cycle's treat half in the same decision, so it needs four.
-constexpr int NACC = 4;
+// cycle's fire half and the previous cycle's treat half in the same decision, so it needs four;
+// the lagged-decision kernel (blocks up to two cycles apart) needs seven (k_wheel_lag).
+constexpr int NACC = 8;
 struct Acc {                       // per-cycle accumulators, slot c % NACC
   unsigned n_act;                  // entries appended to the next active list
   unsigned n_pool;                 // phantoms appended to the next pool (may exceed capacity)
@@ -125,6 +126,7 @@ struct Acc {                       // per-cycle accumulators, slot c % NACC
   unsigned long long live;         // sweep: live lanes at the top of the cycle (E); wheel: lanes started
   unsigned long long arrivals, created, relabels, triggered, started, tested;
   long long pend_lanes, pend_phantoms;   // timing wheel: events in flight at the top of this cycle
+  unsigned nfire, pad_;            // lagged-decision kernel: blocks that finished this cycle's fire
 };
 
 // A slab's proposal for the decision of one cycle; the slabs' proposals are
@@ -423,6 +425,14 @@ template <int D> __device__ __forceinline__ typename Tr<D>::LW load_f2(const Dev
 // ---------------------------------------------------------------------------
 // Shared memory (dynamic; one layout for every kernel)
 // ---------------------------------------------------------------------------
+struct LagState {                  // k_wheel_lag: the decision chain (identical in every block)
+  long long pl, pp;                // events in flight at the top of the next cycle to decide
+  unsigned dn;                     // next cycle to decide
+  unsigned ncount, pad_;           // counted cycles so far; the last decided cycle was counted
+  unsigned region, lmode;          // the latest decision's parameters for the next views
+  int status;                      // ST_RUNNING or the terminal status
+};
+
 struct Smem {
   unsigned long long qp[QP_CAP];   // phantom / event staging (wheel: delay in bits 56..63)
   unsigned qa[QA_CAP];             // active-list staging
@@ -460,6 +470,7 @@ struct Smem {
   unsigned long long stg_bar;      // mbarrier of the bulk copy
   unsigned stg_lo, stg_n, stg_phase;
 #endif
+  LagState lag;                    // k_wheel_lag only
 };
 
 __device__ __forceinline__ Smem& smem() {
@@ -1381,6 +1392,7 @@ __device__ __forceinline__ void reset_acc(Acc* a) {
   a->n_act = 0; a->n_pool = 0; a->tl_over = 0; a->tl_total = 0; a->dmin = 0xFFFFFFFFu;
   a->bhit = 0; a->live = 0; a->arrivals = 0; a->created = 0; a->relabels = 0; a->triggered = 0;
   a->started = 0; a->tested = 0; a->pend_lanes = 0; a->pend_phantoms = 0;
+  a->nfire = 0;
 }
 
 __device__ __forceinline__ void resolve_hit(const Dev& s, unsigned long long bhit, long long t, unsigned c) {

@@ -1154,6 +1154,221 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_hybrid(Dev s) {
 }
 
 // ---------------------------------------------------------------------------
+// Lagged-decision wheel kernel (single device, dense wheel cycles; the default where the hybrid
+// applies).  The hybrid kernel still meets the whole grid after every fire, because the decision
+// for cycle c (a target reached, nothing in flight, an overflow, the budget) needs the complete
+// fire(c).  Here no cycle waits for its own decision:
+//   * time steps by one every cycle (t(c) = c; a cycle whose bucket is empty fires nothing and is
+//     not counted, so outputs and counters are those of the jumping wheel, i.e. tier 5's);
+//   * treat(c) waits only for the fire(c) of the blocks within hyb_R, fire(c + 1) only for their
+//     treat(c) (progress words: 2c + 1 = fire(c) done, 2c + 2 = treat(c) done);
+//   * decision x is taken by every block (identically, in order) once every block has counted
+//     its fire(x) in slot x (nfire == G), i.e. between fire(x + 1) and treat(x + 1): the block's own
+//     next cycle overlaps the slowest block's fire instead of waiting for it;
+//   * cycles that need the whole grid's fire(c) before treat(c) (sparse cycles, whose treat walks
+//     the global list, and the f1max time units after one, whose fires write far from their
+//     slabs) take decision c before treat(c), as the hybrid does.
+// A terminating decision x is seen after fire(x + 1) ran: that fire is discarded (its counters
+// sit in slot x + 1, which no decision reads; it writes no target list of cycle x; an overflow it
+// could flag carries a later time).  Blocks are at most two cycles apart (fire(c + 2) anywhere
+// needs decision c, which needs every fire(c)); hence NACC >= 7, the reset of slot c + 2 and of
+// the bucket of cycle c - 5 at block 0's fire(c), and ring heads recorded for cycle c + 1 there.
+// ---------------------------------------------------------------------------
+static_assert(NACC >= 7, "k_wheel_lag: slots of cycles up to two apart plus their readers");
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wheel_cycle_start_lag(const Dev& s, const View& v) {
+  reset_acc(&s.ctl->acc[(v.c + 2) % NACC]);
+  if (v.c >= 5) {                  // last read by decision c - 4, which every block has taken
+    const unsigned b5 = (v.c - 5) & (WHEEL - 1);
+    s.bnev[b5] = 0; s.bnlane[b5] = 0;
+  }
+  s.ctl->hist_t[v.c & (WHEEL - 1)] = v.t;
+  // every event allocated before this point comes from a treat of cycle <= c (treat(c + 1)
+  // anywhere needs decision c, i.e. this block's fire(c))
+  s.ctl->hist_head[(v.c + 1) & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
+}
+
+// Decision of cycle x = L.dn (warp 0; lane 0 updates L; lane 0 of block 0 writes the totals).
+// Inputs: fire(x) (slot x), treat(x - 1) (slot x - 1) and the bucket counts of cycles x, x - 1 —
+// all final once every block has counted fire(x).
+__device__ void decide_lag(const Dev& s, LagState& L, bool writer) {
+  const unsigned lane = threadIdx.x & 31u;
+  Ctl* C = s.ctl;
+  const unsigned x = L.dn;
+  const long long t = (long long)x;
+  Acc* a = &C->acc[x % NACC];
+  Acc* ap = &C->acc[(x + NACC - 1) % NACC];
+  if (lane == 0) {
+    const unsigned b = (unsigned)(t & (WHEEL - 1)), bp = (unsigned)((t - 1) & (WHEEL - 1));
+    const long long fired = x > 0 ? (long long)__ldcg(s.bnev + b) : 0;
+    const long long fp = x > 1 ? (long long)__ldcg(s.bnev + bp) : 0;
+    const long long fpl = x > 1 ? (long long)__ldcg(s.bnlane + bp) : 0;
+    const unsigned long long bhit = x > 0 ? __ldcg(&a->bhit) : 0ull;
+    const unsigned long long started = __ldcg(&ap->started), created = __ldcg(&ap->created);
+    const unsigned long long triggered = __ldcg(&ap->triggered);
+    const long long ovft = __ldcg((const long long*)&C->ovf_t);
+    long long pl = 0, pp = 0;                         // events in flight at the top of cycle x
+    if (x > 0) {
+      pl = L.pl - fpl + (long long)started;
+      pp = L.pp - (fp - fpl) + (long long)created;
+    }
+    const bool counted = x > 0 && (s.unit || fired > 0);
+    if (writer) {
+      if (counted) { C->cycles += 1; C->edge_updates += pl + pp; }
+      C->arrivals += __ldcg(&a->arrivals);
+      C->triggered += triggered; C->created += created;
+      C->relabels += __ldcg(&ap->relabels); C->started += started;
+      if (pl + pp > C->peak_phantoms) C->peak_phantoms = pl + pp;
+    }
+    L.pl = pl; L.pp = pp;
+    L.ncount += counted ? 1u : 0u;
+    L.pad_ = counted ? 1u : 0u;
+    int st = ST_RUNNING;
+    if (bhit) {
+      st = 0;                                         // the target reached (reading R-new-3)
+      if (writer) resolve_hit(s, bhit, t, x);
+    } else if (x > 0 && ovft < t) {
+      st = 8;                                         // an overflow of treat(x - 1) or earlier
+      if (writer) {
+        // live events: those of cycles c' with c' + f1max > x, allocated after hist_head[c' + 1]
+        const long long cd = (long long)x - s.f1max;  // newest cycle whose events all fired
+        const unsigned long long oldest = cd >= 0 ? __ldcg(&C->hist_head[(cd + 1) & (WHEEL - 1)]) : 0ull;
+        C->need_pool = __ldcg(&C->wheel_overflow) & 2u ? -2 : (long long)(__ldcg(&C->ev_head) - oldest) + 1;
+      }
+    } else if (x > 0 && pl + pp == 0) {
+      st = 1;                                         // nothing was in flight at the top of cycle x
+    } else if (s.budget > 0 && (long long)L.ncount >= s.budget) {
+      st = 4;
+    } else {
+      const unsigned long long per = (started + created) * 2ull /
+                                     ((unsigned long long)s.nblocks * (unsigned long long)max(1, s.f1max));
+      unsigned r = 128;
+      while (r < per && r < 4096u) r <<= 1;
+      if (x > 0) L.region = r;
+      L.lmode = triggered <= s.list_max && x > 0;
+    }
+    L.status = st;
+    if (writer && st != ST_RUNNING) {
+      View nv{};
+      nv.t = t; nv.c = x; nv.stamp = stamp_of(x); nv.delta = 1; nv.status = st;
+      nv.region = L.region; nv.lmode = L.lmode; nv.ncount = L.ncount; nv.pad_ = L.pad_;
+      C->view = nv;
+    }
+    L.dn = x + 1;
+  }
+  __syncwarp();
+}
+
+// Take the decisions up to cycle `upto` (warp 0 waits for each cycle's fire count).  False: abort.
+__device__ bool decide_upto(const Dev& s, Smem& sm, unsigned upto) {
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    const unsigned G = gridDim.x;
+    unsigned ok = 1;
+    for (;;) {
+      __syncwarp();
+      const unsigned x = sm.lag.dn;
+      if (x > upto || sm.lag.status != ST_RUNNING) break;
+      if (x > 0) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (!__all_sync(0xFFFFFFFFu, ld_acquire_u32(&s.ctl->acc[x % NACC].nfire) >= G)) {
+          __nanosleep(32);
+          unsigned bad = 0;
+          if (lane == 0) {
+            if (*(volatile unsigned*)&s.ctl->abort) bad = 1;
+            else if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&s.ctl->abort, 1u); bad = 1; }
+          }
+          if (__shfl_sync(0xFFFFFFFFu, bad, 0)) { ok = 0; break; }
+        }
+        if (!ok) break;
+      }
+      decide_lag(s, sm.lag, blockIdx.x == 0);
+    }
+    if (lane == 0) sm.flag = ok;
+  }
+  __syncthreads();
+  const bool ok = sm.flag != 0;
+  __syncthreads();
+  return ok;
+}
+
+template <int D, int MINB = WCSP_MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_wheel_lag(Dev s) {
+  Smem& sm = smem();
+  init_smem(sm);
+  View v;
+  load_view(s, sm, v);             // c = 0, t = 0: the treatment of A
+  if (threadIdx.x == 0) {
+    LagState& L = sm.lag;
+    L.pl = 0; L.pp = 0; L.dn = v.c; L.ncount = v.ncount; L.pad_ = v.pad_;
+    L.region = v.region; L.lmode = v.lmode; L.status = ST_RUNNING;
+  }
+  __syncthreads();
+  const unsigned long long G = gridDim.x;
+  unsigned long long target = 0;   // grid_sync counter (after sparse treats, maintenance)
+  bool glob = true;                // the previous treat ended with a grid barrier (or there was none)
+  long long t_list = -(1ll << 40); // time of the last listed (sparse) treat (see k_wheel_hybrid)
+  for (;;) {
+    const unsigned c = v.c;
+    const bool sync = v.lmode || v.t <= t_list + s.f1max;   // treat(c) needs the whole grid's fire(c)
+    if (c > 0) {
+      if (!glob) {
+        if (s.hyb_prep) {          // own-data prologue first: its loads overlap the neighbourhood wait
+          if (MINB < 4 && v.lmode) fire_prologue<D, false, FIRE_ITEMS>(s, v, sm);
+          else fire_prologue<D, false, fire_items<MINB>()>(s, v, sm);
+        }
+        if (!local_wait(s, sm, 2ull * c)) return;
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) wheel_cycle_start_lag(s, v);
+      if (MINB < 4 && v.lmode) wheel_fire<D, false, FIRE_ITEMS>(s, v, sm);
+      else wheel_fire<D, false, fire_items<MINB>()>(s, v, sm);
+      __syncthreads();
+      if (threadIdx.x == 0) {      // count fire(c) in its slot, publish it to the neighbourhood
+        __threadfence();
+        atomicAdd(&s.ctl->acc[c % NACC].nfire, 1u);
+        st_release_gpu(s.prog + blockIdx.x, 2ull * c + 1);
+      }
+    }
+    // decisions up to c - 1 (up to c before a treat that needs the whole fire(c), and at c = 0)
+    if (!decide_upto(s, sm, (c == 0 || sync) ? c : c - 1)) return;
+    if (sm.lag.status != ST_RUNNING) break;
+    if (c > 0 && !sync && !local_wait(s, sm, 2ull * c + 1)) return;
+    if (threadIdx.x == 0) {        // ring: events of cycles c' with c' + f1max >= c may still be read
+      const long long cd = (long long)c - 1 - s.f1max;
+      const unsigned long long oldest = cd >= 0 ? __ldcg(&s.ctl->hist_head[(cd + 1) & (WHEEL - 1)]) : 0ull;
+      sm.alloc_lim = oldest + s.ev_mask + 1;
+    }
+    __syncthreads();
+    phase_treat<D, true>(s, v, sm);                     // treat(c) with cycle c's view
+    if (v.lmode) t_list = v.t;
+    View nv = v;
+    nv.c = c + 1; nv.t = v.t + 1; nv.delta = 1; nv.stamp = stamp_of(c + 1);
+    nv.region = sm.lag.region; nv.lmode = sm.lag.lmode;
+    const bool maint = nv.stamp == 1u || (nv.t / MAINT_PERIOD_T) != (v.t / MAINT_PERIOD_T);
+    if (v.lmode || maint || nv.t <= t_list + s.f1max) {  // listed vertices / their events / maint
+      target += G;
+      if (!grid_sync(s.ctl, target, sm)) return;
+      if (maint) {
+        wheel_maintain(s, nv.t);
+        target += G;
+        if (!grid_sync(s.ctl, target, sm)) return;
+      }
+      glob = true;
+    } else {
+      publish_treat(s, 2ull * c + 2);
+      glob = false;
+    }
+    v = nv;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Peer halo: every slab runs the persistent wheel cycle in
 // ONE cooperative kernel per device, and the halo is fused into it — water
 // that crosses a slab boundary is a system-scope atomicMax straight into the

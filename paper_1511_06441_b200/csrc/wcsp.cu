@@ -253,6 +253,12 @@ Dev make_dev(const wcsp_handle* h) {
   s.prog = h->prog;
   s.hyb_R = h->hyb_R;
   s.hyb_prep = getenv("WCSP_HYB_PREP") ? atoi(getenv("WCSP_HYB_PREP")) != 0 : 1;   // A/B switch
+  // k_wheel_lag: decision c - 1 before treat(c) while the state words fit in a few L2s (C3 124.5 ->
+  // 122.5 ms, C2 90.4 -> 85.4 ms), after it on DRAM-resident grids, whose fires are too uneven to
+  // make treat(c) wait for the slowest block's fire(c - 1) (C5z8 6.98 -> 6.66 s;
+  // profiles/r02/ab_lag_pre.txt)
+  s.lag_pre = getenv("WCSP_LAG_PRE") ? atoi(getenv("WCSP_LAG_PRE")) != 0
+                                     : 8.0 * (double)h->N <= 4.0 * (double)std::max<long long>(h->l2_bytes, 1);
   // sparse cycles: about 64 triggered vertices per block (WCSP_LIST_MAX overrides, A/B runs)
   s.list_max = getenv("WCSP_LIST_MAX") ? strtoull(getenv("WCSP_LIST_MAX"), nullptr, 10)
                                        : (unsigned long long)h->grid * 64ull;

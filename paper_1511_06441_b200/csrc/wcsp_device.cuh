@@ -228,6 +228,7 @@ struct Dev {
   unsigned long long* prog;        // [nblocks] treats completed (monotone per solve)
   int hyb_R;
   int hyb_prep;                    // run the fire's own-data prologue before the neighbourhood wait
+  int lag_pre;                     // k_wheel_lag A/B: decision c - 1 before treat(c) instead of after
   // slab partition (multi-GPU / virtual slabs): local index + goff = global index
   unsigned goff;
   unsigned plane;                  // vertices per plane of the partitioned (last) axis

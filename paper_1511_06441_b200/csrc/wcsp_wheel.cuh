@@ -1163,16 +1163,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_hybrid(Dev s) {
 //   * treat(c) waits only for the fire(c) of the blocks within hyb_R, fire(c + 1) only for their
 //     treat(c) (progress words: 2c + 1 = fire(c) done, 2c + 2 = treat(c) done);
 //   * decision x is taken by every block (identically, in order) once every block has counted
-//     its fire(x) in slot x (nfire == G), i.e. between fire(x + 1) and treat(x + 1): the block's own
-//     next cycle overlaps the slowest block's fire instead of waiting for it;
+//     its fire(x) in slot x (nfire == G), after the block's treat(x + 1) and before its fire(x + 2):
+//     the decision's loads overlap the wait for the neighbours' treats, and no block waits for the
+//     slowest block's fire of its own cycle;
 //   * cycles that need the whole grid's fire(c) before treat(c) (sparse cycles, whose treat walks
 //     the global list, and the f1max time units after one, whose fires write far from their
 //     slabs) take decision c before treat(c), as the hybrid does.
-// A terminating decision x is seen after fire(x + 1) ran: that fire is discarded (its counters
-// sit in slot x + 1, which no decision reads; it writes no target list of cycle x; an overflow it
-// could flag carries a later time).  Blocks are at most two cycles apart (fire(c + 2) anywhere
-// needs decision c, which needs every fire(c)); hence NACC >= 7, the reset of slot c + 2 and of
-// the bucket of cycle c - 5 at block 0's fire(c), and ring heads recorded for cycle c + 1 there.
+// A terminating decision x is seen after fire(x + 1) and treat(x + 1) ran: they are discarded
+// (their counters sit in slot x + 1, which no decision reads; they write no target list of cycle
+// x; an overflow they flag carries a later time).  Blocks are at most two cycles apart (fire(c + 2)
+// anywhere needs decision c, which needs every fire(c)); hence NACC >= 7, the reset of slot c + 2
+// and of the bucket of cycle c - 5 at block 0's fire(c), and the ring head recorded there for
+// cycle c + 2 (a treat(c + 1) may already be allocating elsewhere).
 // ---------------------------------------------------------------------------
 static_assert(NACC >= 7, "k_wheel_lag: slots of cycles up to two apart plus their readers");
 
@@ -1189,9 +1191,9 @@ __device__ __forceinline__ void wheel_cycle_start_lag(const Dev& s, const View& 
     s.bnev[b5] = 0; s.bnlane[b5] = 0;
   }
   s.ctl->hist_t[v.c & (WHEEL - 1)] = v.t;
-  // every event allocated before this point comes from a treat of cycle <= c (treat(c + 1)
-  // anywhere needs decision c, i.e. this block's fire(c))
-  s.ctl->hist_head[(v.c + 1) & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
+  // every event allocated before this point comes from a treat of cycle <= c + 1 (treat(c + 2)
+  // anywhere follows that block's fire(c + 2), which needs decision c, i.e. this block's fire(c))
+  s.ctl->hist_head[(v.c + 2) & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
 }
 
 // Decision of cycle x = L.dn (warp 0; lane 0 updates L; lane 0 of block 0 writes the totals).
@@ -1236,8 +1238,9 @@ __device__ void decide_lag(const Dev& s, LagState& L, bool writer) {
     } else if (x > 0 && ovft < t) {
       st = 8;                                         // an overflow of treat(x - 1) or earlier
       if (writer) {
-        // live events: those of cycles c' with c' + f1max > x, allocated after hist_head[c' + 1]
-        const long long cd = (long long)x - s.f1max;  // newest cycle whose events all fired
+        // live events: those of cycles after cd = x - f1max (the newest whose events all fired);
+        // hist_head[cd + 1] precedes every allocation of a treat after cd
+        const long long cd = (long long)x - s.f1max;
         const unsigned long long oldest = cd >= 0 ? __ldcg(&C->hist_head[(cd + 1) & (WHEEL - 1)]) : 0ull;
         C->need_pool = __ldcg(&C->wheel_overflow) & 2u ? -2 : (long long)(__ldcg(&C->ev_head) - oldest) + 1;
       }
@@ -1335,17 +1338,29 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_lag(Dev s) {
         st_release_gpu(s.prog + blockIdx.x, 2ull * c + 1);
       }
     }
-    // decisions up to c - 1 (up to c before a treat that needs the whole fire(c), and at c = 0)
-    if (!decide_upto(s, sm, (c == 0 || sync) ? c : c - 1)) return;
-    if (sm.lag.status != ST_RUNNING) break;
-    if (c > 0 && !sync && !local_wait(s, sm, 2ull * c + 1)) return;
-    if (threadIdx.x == 0) {        // ring: events of cycles c' with c' + f1max >= c may still be read
-      const long long cd = (long long)c - 1 - s.f1max;
+    // async cycle: treat(c) after the neighbourhood's fire(c), then decision c - 1 (its latency
+    // overlaps the neighbours' treats); a treat that needs the whole fire(c) (and c = 0) takes the
+    // decisions up to c first
+    const bool early = c == 0 || sync;
+    if (early || s.lag_pre) {      // (lag_pre: A/B of decision c - 1 before treat(c))
+      if (!decide_upto(s, sm, early ? c : c - 1)) return;
+      if (sm.lag.status != ST_RUNNING) break;
+    }
+    if (!early && !local_wait(s, sm, 2ull * c + 1)) return;
+    if (threadIdx.x == 0) {
+      // ring: every block has fired cycles <= c - 2, so events of cycles cd <= c - 2 - f1max are
+      // dead; hist_head[cd + 1] precedes every allocation of a later treat
+      const long long cd = (long long)c - 2 - s.f1max;
       const unsigned long long oldest = cd >= 0 ? __ldcg(&s.ctl->hist_head[(cd + 1) & (WHEEL - 1)]) : 0ull;
       sm.alloc_lim = oldest + s.ev_mask + 1;
     }
     __syncthreads();
     phase_treat<D, true>(s, v, sm);                     // treat(c) with cycle c's view
+    publish_treat(s, 2ull * c + 2);
+    if (!early && !s.lag_pre) {
+      if (!decide_upto(s, sm, c - 1)) return;
+      if (sm.lag.status != ST_RUNNING) break;
+    }
     if (v.lmode) t_list = v.t;
     View nv = v;
     nv.c = c + 1; nv.t = v.t + 1; nv.delta = 1; nv.stamp = stamp_of(c + 1);
@@ -1361,8 +1376,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_lag(Dev s) {
       }
       glob = true;
     } else {
-      publish_treat(s, 2ull * c + 2);
-      glob = false;
+      glob = false;                // treat(c) is published: fire(c + 1) waits for the neighbourhood
     }
     v = nv;
   }

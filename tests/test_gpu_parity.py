@@ -549,16 +549,20 @@ def test_both_cycle_kernel_builds(bps, monkeypatch):
             assert rp.key() == r.key() and model_counters(rp) == model_counters(r), (shape, slabs, rp, r)
 
 
-@pytest.mark.parametrize("hyb", ["1"])
-def test_hybrid_one_barrier_kernel(hyb, monkeypatch):
-    """The one-barrier hybrid kernel (k_wheel_hybrid; WCSP_HYBRID=1 forces it on every
-    single-device persistent wheel solve): neighbourhood waits replace the grid barrier after
-    the treat, time advances by 1 after a fire that delivered water and jumps otherwise, and
-    only non-empty cycles are counted — outputs equal the oracle's and every work counter
-    tier 5's, on random grids (holes, several sources/targets, M = infinity), sparse-cycle
-    runs (the fractal, listed treats), repeated solves (no run-to-run difference), a tiny
-    event ring (the allocation guard and the regrow) and both kernel builds."""
-    monkeypatch.setenv("WCSP_HYBRID", hyb)
+@pytest.mark.parametrize("lag", ["0", "1"])
+def test_hybrid_one_barrier_kernel(lag, monkeypatch):
+    """The neighbourhood-synchronised wheel kernels on every single-device persistent wheel
+    solve (WCSP_HYBRID=1): lag=0 the one-barrier hybrid (k_wheel_hybrid: neighbourhood waits
+    replace the grid barrier after the treat, time advances by 1 after a fire that delivered
+    water and jumps otherwise), lag=1 the lagged-decision kernel (k_wheel_lag: time steps by one,
+    treat(c) waits only for the neighbourhood's fire(c), decision c is taken one cycle later and a
+    terminating one discards the fire that ran past it).  Only non-empty cycles are counted —
+    outputs equal the oracle's and every work counter tier 5's, on random grids (holes, several
+    sources/targets, M = infinity), sparse-cycle runs (the fractal, listed treats), repeated
+    solves (no run-to-run difference), a tiny event ring (the allocation guard and the regrow)
+    and both kernel builds."""
+    monkeypatch.setenv("WCSP_HYBRID", "1")
+    monkeypatch.setenv("WCSP_HYB_LAG", lag)
     rng = np.random.default_rng(4321)
     for i in range(80):
         inst = I.random_small(rng, shapes=[(12, 12), (6, 6, 6), (30, 9), (3, 4, 3, 3), (40,), (16, 16, 16)],

@@ -829,13 +829,15 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
   const unsigned long long cap = opt.phantom_capacity > 0 ? (unsigned long long)opt.phantom_capacity
                                                           : std::max<unsigned long long>(4 * N, 1ull << 20);
   if (is_wheel(opt.engine)) {
-    // auto: twice the sweep pool's default plus the slack of every block's open regions over the
-    // ~f1max cycles a slot stays allocated (grid x 10 delays x 4096-slot regions, twice) — without it
-    // C3's first solve on a fresh handle overflowed the 2^27-slot ring and re-ran — unless the
-    // power-of-two rounding would then double a ring of more than 2^31 slots (C5: 8N alone suffices).
-    // An explicit capacity is taken as given (the overflow path grows it).
+    // auto: twice the sweep pool's default plus the slack of every block's open regions (grid x 10
+    // delays x 4096-slot regions) over the cycles the ring guard keeps them live — eight: the
+    // lagged-decision kernel counts a cycle's slots live until every block has fired two cycles
+    // past their last use (with two, C3's first solve on a fresh handle overflowed the 2^28-slot
+    // ring and re-ran: profiles/r02/first_solve_lag_r02aj.log) — unless the power-of-two rounding
+    // would then double a ring of more than 2^31 slots (C5: 8N alone suffices).  An explicit
+    // capacity is taken as given (the overflow path grows it).
     unsigned long long ring = std::max<unsigned long long>(2 * cap, (unsigned long long)h->grid * 2 * 4096);
-    const unsigned long long slack = std::min<unsigned long long>((unsigned long long)h->grid * 2ull * 10ull * 4096ull,
+    const unsigned long long slack = std::min<unsigned long long>((unsigned long long)h->grid * 8ull * 10ull * 4096ull,
                                                                   4 * cap);   // small grids: small rings
     if (pow2_at_least(ring + slack) <= (1ull << 31)) ring += slack;
     CKH(alloc_ring(h, opt.phantom_capacity > 0 ? cap : ring));

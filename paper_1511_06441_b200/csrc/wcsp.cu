@@ -257,6 +257,9 @@ Dev make_dev(const wcsp_handle* h) {
   // 122.5 ms, C2 90.4 -> 85.4 ms), after it on DRAM-resident grids, whose fires are too uneven to
   // make treat(c) wait for the slowest block's fire(c - 1) (C5z8 6.98 -> 6.66 s;
   // profiles/r02/ab_lag_pre.txt)
+  // k_wheel_lag A/B: warp 1 waits for the neighbourhood beside warp 0's decision (C3 122.6 -> 122.9,
+  // C2 85.3 -> 87.5, C3s 14.3 -> 14.1 ms; profiles/r02/ab_lag_par.txt): off
+  s.lag_par = getenv("WCSP_LAG_PAR") ? atoi(getenv("WCSP_LAG_PAR")) != 0 : 0;
   s.lag_pre = getenv("WCSP_LAG_PRE") ? atoi(getenv("WCSP_LAG_PRE")) != 0
                                      : 8.0 * (double)h->N <= 4.0 * (double)std::max<long long>(h->l2_bytes, 1);
   // sparse cycles: about 64 triggered vertices per block (WCSP_LIST_MAX overrides, A/B runs)

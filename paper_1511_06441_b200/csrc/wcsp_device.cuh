@@ -229,6 +229,7 @@ struct Dev {
   int hyb_R;
   int hyb_prep;                    // run the fire's own-data prologue before the neighbourhood wait
   int lag_pre;                     // k_wheel_lag A/B: decision c - 1 before treat(c) instead of after
+  int lag_par;                     // k_wheel_lag: that decision (warp 0) and the neighbourhood wait (warp 1) together
   // slab partition (multi-GPU / virtual slabs): local index + goff = global index
   unsigned goff;
   unsigned plane;                  // vertices per plane of the partitioned (last) axis
@@ -459,6 +460,7 @@ struct Smem {
   unsigned bm_lo, bm_words;        // wheel fire, dense cycles: the block's triggered bitmap in qp covers
                                    // vertices [bm_lo, bm_lo + 32 * bm_words)
   unsigned base_a, base_b, flag, ovf;
+  unsigned flag2;                  // k_wheel_lag: warp 1's neighbourhood wait beside warp 0's decisions
   unsigned f_nd, f_prep;           // fire: descriptors of this block's bucket; prologue already run
   unsigned long long alloc_lim;    // event-ring allocations of this treat must stay below (hybrid guard)
   View view;

@@ -937,31 +937,37 @@ __device__ __forceinline__ void wheel_cycle_start_hyb(const Dev& s, const View& 
 
 // Neighbourhood wait (warp 0, one progress word per lane, polled together): every block within
 // hyb_R has published prog >= c.
+// One warp polls every block within hyb_R for prog >= c; false if the watchdog fired.
+__device__ __forceinline__ unsigned neigh_wait_warp(const Dev& s, unsigned long long c) {
+  const unsigned lane = threadIdx.x & 31u;
+  const int b = (int)blockIdx.x, G = (int)gridDim.x;
+  const int lo = max(0, b - s.hyb_R), hi = min(G - 1, b + s.hyb_R);
+  const unsigned long long t0 = globaltimer_ns();
+  unsigned ok = 1;
+  for (int j0 = lo; j0 <= hi; j0 += 32) {
+    const int j = j0 + (int)lane;
+    for (;;) {
+      const bool done = j > hi || ld_acquire(s.prog + j) >= c;
+      if (__all_sync(0xFFFFFFFFu, done)) break;
+      __nanosleep(32);
+      unsigned bad = 0;
+      if (lane == 0) {
+        if (*(volatile unsigned*)&s.ctl->abort) bad = 1;
+        else if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&s.ctl->abort, 1u); bad = 1; }
+      }
+      if (__shfl_sync(0xFFFFFFFFu, bad, 0)) { ok = 0; break; }
+    }
+    if (!ok) break;
+  }
+  __threadfence();
+  return ok;
+}
+
 __device__ __forceinline__ bool local_wait(const Dev& s, Smem& sm, unsigned long long c) {
   __syncthreads();
   if (threadIdx.x < 32) {
-    const unsigned lane = threadIdx.x;
-    const int b = (int)blockIdx.x, G = (int)gridDim.x;
-    const int lo = max(0, b - s.hyb_R), hi = min(G - 1, b + s.hyb_R);
-    const unsigned long long t0 = globaltimer_ns();
-    unsigned ok = 1;
-    for (int j0 = lo; j0 <= hi; j0 += 32) {
-      const int j = j0 + (int)lane;
-      for (;;) {
-        const bool done = j > hi || ld_acquire(s.prog + j) >= c;
-        if (__all_sync(0xFFFFFFFFu, done)) break;
-        __nanosleep(32);
-        unsigned bad = 0;
-        if (lane == 0) {
-          if (*(volatile unsigned*)&s.ctl->abort) bad = 1;
-          else if (globaltimer_ns() - t0 > BARRIER_TIMEOUT_NS) { atomicExch(&s.ctl->abort, 1u); bad = 1; }
-        }
-        if (__shfl_sync(0xFFFFFFFFu, bad, 0)) { ok = 0; break; }
-      }
-      if (!ok) break;
-    }
-    __threadfence();
-    if (lane == 0) sm.flag = ok;
+    const unsigned ok = neigh_wait_warp(s, c);
+    if (threadIdx.x == 0) sm.flag = ok;
   }
   __syncthreads();
   const bool ok = sm.flag != 0;
@@ -1268,8 +1274,13 @@ __device__ void decide_lag(const Dev& s, LagState& L, bool writer) {
   __syncwarp();
 }
 
-// Take the decisions up to cycle `upto` (warp 0 waits for each cycle's fire count).  False: abort.
-__device__ bool decide_upto(const Dev& s, Smem& sm, unsigned upto) {
+// Take the decisions up to cycle `upto` (warp 0 waits for each cycle's fire count) and, if
+// wait_c > 0, wait for the neighbourhood's prog >= wait_c at the same time (warp 1).  False: abort.
+__device__ bool decide_upto(const Dev& s, Smem& sm, unsigned upto, unsigned long long wait_c = 0) {
+  if (wait_c > 0 && threadIdx.x >= 32 && threadIdx.x < 64) {
+    const unsigned ok = neigh_wait_warp(s, wait_c);
+    if (threadIdx.x == 32) sm.flag2 = ok;
+  }
   if (threadIdx.x < 32) {
     const unsigned lane = threadIdx.x;
     const unsigned G = gridDim.x;
@@ -1296,7 +1307,7 @@ __device__ bool decide_upto(const Dev& s, Smem& sm, unsigned upto) {
     if (lane == 0) sm.flag = ok;
   }
   __syncthreads();
-  const bool ok = sm.flag != 0;
+  const bool ok = sm.flag != 0 && (wait_c == 0 || sm.flag2 != 0);
   __syncthreads();
   return ok;
 }
@@ -1342,11 +1353,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_lag(Dev s) {
     // overlaps the neighbours' treats); a treat that needs the whole fire(c) (and c = 0) takes the
     // decisions up to c first
     const bool early = c == 0 || sync;
-    if (early || s.lag_pre) {      // (lag_pre: A/B of decision c - 1 before treat(c))
-      if (!decide_upto(s, sm, early ? c : c - 1)) return;
+    if (early) {
+      if (!decide_upto(s, sm, c)) return;
       if (sm.lag.status != ST_RUNNING) break;
-    }
-    if (!early && !local_wait(s, sm, 2ull * c + 1)) return;
+    } else if (s.lag_pre) {        // decision c - 1 (warp 0) beside the wait for the neighbours' fire(c)
+      if (!decide_upto(s, sm, c - 1, s.lag_par ? 2ull * c + 1 : 0ull)) return;
+      if (sm.lag.status != ST_RUNNING) break;
+      if (!s.lag_par && !local_wait(s, sm, 2ull * c + 1)) return;
+    } else if (!local_wait(s, sm, 2ull * c + 1)) return;
     if (threadIdx.x == 0) {
       // ring: every block has fired cycles <= c - 2, so events of cycles cd <= c - 2 - f1max are
       // dead; hist_head[cd + 1] precedes every allocation of a later treat

@@ -476,9 +476,9 @@ def run_ours(args, rank, world, local):
         if world > 1:
             et, e_upd = reduce_timing(et, e_upd / world if slabs else e_upd, "cuda")
         e2e = {"value": e_upd / (et / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": 6656, "ms_per_step": et / args.e2e_steps,
+               "d2h_bytes_per_step": 5760, "ms_per_step": et / args.e2e_steps,
                "path": "wcsp_load (pinned host f1,f2,A,B -> HBM, validate, weight build) + wcsp_solve + result "
-                       "D2H (the 6656-byte control block, sizeof(Ctl))"}
+                       "D2H (the 5760-byte control block, sizeof(Ctl))"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

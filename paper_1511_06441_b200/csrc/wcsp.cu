@@ -259,7 +259,6 @@ Dev make_dev(const wcsp_handle* h) {
   // profiles/r02/ab_lag_pre.txt)
   // k_wheel_lag A/B: warp 1 waits for the neighbourhood beside warp 0's decision (C3 122.6 -> 122.9,
   // C2 85.3 -> 87.5, C3s 14.3 -> 14.1 ms; profiles/r02/ab_lag_par.txt): off
-  s.lag_k = getenv("WCSP_LAG_K") ? std::min(3, std::max(1, atoi(getenv("WCSP_LAG_K")))) : 1;
   s.lag_par = getenv("WCSP_LAG_PAR") ? atoi(getenv("WCSP_LAG_PAR")) != 0 : 0;
   s.lag_pre = getenv("WCSP_LAG_PRE") ? atoi(getenv("WCSP_LAG_PRE")) != 0
                                      : 8.0 * (double)h->N <= 4.0 * (double)std::max<long long>(h->l2_bytes, 1);
@@ -358,7 +357,7 @@ wcsp_status validate_device(wcsp_handle* h, const uint8_t* f1, const uint8_t* f2
     if (h->barr) cudaFree(h->barr);
     h->barr = nullptr;
     h->barr_cap = 0;
-    CK(cudaMalloc(&h->barr, (size_t)NBL * need * sizeof(BArr)));   // one list per cycle mod NBL
+    CK(cudaMalloc(&h->barr, 2 * need * sizeof(BArr)));   // one list per cycle parity
     h->barr_cap = (unsigned)need;
   }
   return WCSP_REACHED;
@@ -408,7 +407,7 @@ wcsp_status load_problem(wcsp_handle* h, const wcsp_problem* p) {
     if (need > h->barr_cap) {
       if (h->barr) cudaFree(h->barr);
       h->barr = nullptr;
-      CK(cudaMalloc(&h->barr, (size_t)NBL * need * sizeof(BArr)));
+      CK(cudaMalloc(&h->barr, 2 * need * sizeof(BArr)));
       h->barr_cap = (unsigned)need;
     }
   }

@@ -114,12 +114,8 @@ struct BArr { unsigned D, cand, src, via; };   // an arrival at a target (termin
 // Per-cycle accumulators live in NACC slots (slot c % NACC).  The two-barrier kernels need three
 // (the next cycle's slot is reset while this one is read); the one-barrier hybrid kernel reads a
 // cycle's fire half and the previous cycle's treat half in the same decision, so it needs four;
-// the lagged-decision kernel with decision lag K (blocks up to K + 1 cycles apart) needs 3K + 4
-// (k_wheel_lag).
-constexpr int NACC = 16;
-// B-arrival lists (the terminating cycle's arrivals at targets), one per cycle mod NBL: a run that
-// detects its termination k cycles late (k_wheel_lag) must not have overwritten that cycle's list.
-constexpr int NBL = 4;
+// the lagged-decision kernel (blocks up to two cycles apart) needs seven (k_wheel_lag).
+constexpr int NACC = 8;
 struct Acc {                       // per-cycle accumulators, slot c % NACC
   unsigned n_act;                  // entries appended to the next active list
   unsigned n_pool;                 // phantoms appended to the next pool (may exceed capacity)
@@ -155,7 +151,7 @@ struct Ctl {
   unsigned long long bar;          // grid barrier arrivals (persistent engines)
   unsigned long long rel;          // peer halo: epoch released by this slab's leader block
   unsigned abort, pad1_;           // barrier watchdog fired
-  unsigned n_barr2[NBL];           // B-arrival list length per cycle (list c % NBL at barr[(c % NBL) * barr_cap])
+  unsigned n_barr2[2];             // B-arrival list length per cycle parity (list c & 1 at barr[(c & 1) * barr_cap])
   long long F1, F2, X, Y;
   long long via;
   long long cycles, edge_updates, arrivals, triggered, created, relabels, started;
@@ -233,7 +229,6 @@ struct Dev {
   int hyb_R;
   int hyb_prep;                    // run the fire's own-data prologue before the neighbourhood wait
   int lag_pre;                     // k_wheel_lag A/B: decision c - 1 before treat(c) instead of after
-  int lag_k;                       // k_wheel_lag: decision lag in cycles (1..3; blocks up to lag_k + 1 apart)
   int lag_par;                     // k_wheel_lag: that decision (warp 0) and the neighbourhood wait (warp 1) together
   // slab partition (multi-GPU / virtual slabs): local index + goff = global index
   unsigned goff;
@@ -652,7 +647,7 @@ __device__ __forceinline__ void arrive_post(const Dev& s, const View& v, Acc* ac
       const Loc L = locate<PEER>(s, D);
       const unsigned Dg = L.idx + L.goff;
       atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - Dg));
-      const unsigned par = v.c & (NBL - 1u);
+      const unsigned par = v.c & 1u;
       const unsigned k = atomicAdd(&s.ctl->n_barr2[par], 1u);
       if (k < s.barr_cap) s.barr[(size_t)par * s.barr_cap + k] = BArr{Dg, (unsigned)cand, src, via};
     } else if (!PEER && old >= TMP_GHOST) {   // D belongs to a neighbouring slab: hand the water to its owner
@@ -695,7 +690,7 @@ __device__ __forceinline__ void arrive_post_w(const Dev& s, const View& v, Acc* 
     if (old == TMPW_B) {           // termination 1°
       const unsigned Dg = D + s.goff;
       atomicMax(&acc->bhit, ((unsigned long long)(unsigned)cand << 32) | (0xFFFFFFFFu - Dg));
-      const unsigned par = v.c & (NBL - 1u);
+      const unsigned par = v.c & 1u;
       const unsigned k = atomicAdd(&s.ctl->n_barr2[par], 1u);
       if (k < s.barr_cap) s.barr[(size_t)par * s.barr_cap + k] = BArr{Dg, (unsigned)cand, src, via};
     }
@@ -1408,7 +1403,7 @@ __device__ __forceinline__ void resolve_hit(const Dev& s, unsigned long long bhi
   const unsigned q = (unsigned)(bhit >> 32);
   const unsigned X = 0xFFFFFFFFu - (unsigned)bhit;
   // Y = smallest source among cycle c's arrivals at X carrying q; a regular edge wins over a phantom (R5)
-  const unsigned par = c & (NBL - 1u);
+  const unsigned par = c & 1u;
   const unsigned nb = min(__ldcg(&C->n_barr2[par]), s.barr_cap);
   unsigned long long best = ~0ull;
   for (unsigned k = 0; k < nb; ++k) {

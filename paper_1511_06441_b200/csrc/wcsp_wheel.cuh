@@ -301,7 +301,7 @@ __device__ __forceinline__ void wheel_cycle_start(const Dev& s, const View& v) {
   // staircase: target arrivals are resolved per cycle; the list of the previous cycle's parity (read by
   // its decide, which this thread ran) is emptied for the next cycle — the fires of THIS cycle, which
   // other blocks may already have started, append to the other parity's list
-  if (s.staircase) s.ctl->n_barr2[(v.c + 1) & (NBL - 1)] = 0;
+  if (s.staircase) s.ctl->n_barr2[(v.c + 1) & 1] = 0;
   unsigned long long* nf = &s.ctl->fin[(v.c + 1) & 1][0][0];
   nf[0] = 0; nf[1] = 0; nf[2] = 0; nf[3] = 0;
   const unsigned prev = (unsigned)((v.t - v.delta) & (WHEEL - 1));   // the bucket fired last cycle
@@ -1175,16 +1175,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_hybrid(Dev s) {
 //   * cycles that need the whole grid's fire(c) before treat(c) (sparse cycles, whose treat walks
 //     the global list, and the f1max time units after one, whose fires write far from their
 //     slabs) take decision c before treat(c), as the hybrid does.
-// With decision lag K (decision c - K taken in cycle c; K = 1 by default, WCSP_LAG_K) a terminating
-// decision x is seen after fires x + 1 .. x + K (and the treats between) ran: they are discarded
-// (their counters sit in later slots, which no decision reads; they write other target lists —
-// NBL = 4 > K; an overflow they flag carries a later time).  Blocks are at most K + 1 cycles apart
-// (fire(c + K + 1) anywhere needs decision c, which needs every fire(c)); hence NACC >= 3K + 4, the
-// reset of slot c + K + 1 and of the bucket of cycle c - 2K - 3 at block 0's fire(c), and the ring
-// head recorded there for cycle c + K (+ 1 when the decision follows the treat).
+// A terminating decision x is seen after fire(x + 1) and treat(x + 1) ran: they are discarded
+// (their counters sit in slot x + 1, which no decision reads; they write no target list of cycle
+// x; an overflow they flag carries a later time).  Blocks are at most two cycles apart (fire(c + 2)
+// anywhere needs decision c, which needs every fire(c)); hence NACC >= 7, the reset of slot c + 2
+// and of the bucket of cycle c - 5 at block 0's fire(c), and the ring head recorded there for
+// cycle c + 2 (a treat(c + 1) may already be allocating elsewhere).
 // ---------------------------------------------------------------------------
-static_assert(NACC >= 3 * 3 + 4, "k_wheel_lag: decision lag up to 3 needs 3K + 4 accumulator slots");
-static_assert(NBL > 3, "k_wheel_lag: the fires run past a terminating cycle must not reuse its target list");
+static_assert(NACC >= 7, "k_wheel_lag: slots of cycles up to two apart plus their readers");
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -1192,20 +1190,16 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-// Block 0 at the start of fire(c), decision lag K: every block has taken the decisions up to
-// c - 2 - 2K (it finished fire(c - 1 - K)), and no fire(c + K + 1) has started anywhere.
 __device__ __forceinline__ void wheel_cycle_start_lag(const Dev& s, const View& v) {
-  const unsigned K = (unsigned)s.lag_k;
-  reset_acc(&s.ctl->acc[(v.c + K + 1) % NACC]);   // last read by decision c + K + 2 - NACC <= c - 2 - 2K
-  if (v.c >= 2 * K + 3) {                          // last read by decision c - 2 - 2K
-    const unsigned bk = (v.c - 2 * K - 3) & (WHEEL - 1);
-    s.bnev[bk] = 0; s.bnlane[bk] = 0;
+  reset_acc(&s.ctl->acc[(v.c + 2) % NACC]);
+  if (v.c >= 5) {                  // last read by decision c - 4, which every block has taken
+    const unsigned b5 = (v.c - 5) & (WHEEL - 1);
+    s.bnev[b5] = 0; s.bnlane[b5] = 0;
   }
   s.ctl->hist_t[v.c & (WHEEL - 1)] = v.t;
-  // every event allocated before this point comes from a treat of cycle <= c + K - 1 (decision
-  // before the treat) or <= c + K (after it): a treat(z) anywhere follows decision z - K (z - 1 - K),
-  // which needs this block's fire(z - K) (fire(z - 1 - K))
-  s.ctl->hist_head[(v.c + K + (s.lag_pre ? 0u : 1u)) & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
+  // every event allocated before this point comes from a treat of cycle <= c + 1 (treat(c + 2)
+  // anywhere follows that block's fire(c + 2), which needs decision c, i.e. this block's fire(c))
+  s.ctl->hist_head[(v.c + 2) & (WHEEL - 1)] = *(volatile unsigned long long*)&s.ctl->ev_head;
 }
 
 // Decision of cycle x = L.dn (warp 0; lane 0 updates L; lane 0 of block 0 writes the totals).
@@ -1362,24 +1356,23 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_lag(Dev s) {
     if (early) {
       if (!decide_upto(s, sm, c)) return;
       if (sm.lag.status != ST_RUNNING) break;
-    } else if (s.lag_pre && c >= (unsigned)s.lag_k) {   // decision c - K before treat(c)
-      if (!decide_upto(s, sm, c - s.lag_k, s.lag_par ? 2ull * c + 1 : 0ull)) return;
+    } else if (s.lag_pre) {        // decision c - 1 (warp 0) beside the wait for the neighbours' fire(c)
+      if (!decide_upto(s, sm, c - 1, s.lag_par ? 2ull * c + 1 : 0ull)) return;
       if (sm.lag.status != ST_RUNNING) break;
       if (!s.lag_par && !local_wait(s, sm, 2ull * c + 1)) return;
     } else if (!local_wait(s, sm, 2ull * c + 1)) return;
     if (threadIdx.x == 0) {
-      // ring: every block has fired the cycles up to c - K (decision before the treat) or c - K - 1,
-      // so events of cycles cd <= that - f1max are dead; hist_head[cd + 1] precedes every
-      // allocation of a later treat
-      const long long cd = (long long)c - s.lag_k - (s.lag_pre || early ? 0 : 1) - s.f1max;
+      // ring: every block has fired cycles <= c - 2, so events of cycles cd <= c - 2 - f1max are
+      // dead; hist_head[cd + 1] precedes every allocation of a later treat
+      const long long cd = (long long)c - 2 - s.f1max;
       const unsigned long long oldest = cd >= 0 ? __ldcg(&s.ctl->hist_head[(cd + 1) & (WHEEL - 1)]) : 0ull;
       sm.alloc_lim = oldest + s.ev_mask + 1;
     }
     __syncthreads();
     phase_treat<D, true>(s, v, sm);                     // treat(c) with cycle c's view
     publish_treat(s, 2ull * c + 2);
-    if (!early && !s.lag_pre && c >= (unsigned)s.lag_k) {
-      if (!decide_upto(s, sm, c - s.lag_k)) return;
+    if (!early && !s.lag_pre) {
+      if (!decide_upto(s, sm, c - 1)) return;
       if (sm.lag.status != ST_RUNNING) break;
     }
     if (v.lmode) t_list = v.t;

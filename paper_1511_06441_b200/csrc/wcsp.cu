@@ -796,11 +796,13 @@ wcsp_status create_impl(const wcsp_problem* p, const wcsp_options& opt, const Sl
     default: CKC(set_smem_attrs<4>()); break;
   }
   // Persistent wheel engine: the build for 4 resident blocks per SM (64 registers) on 3-D and
-  // higher grids of at least 2^21 vertices (thick fronts: C3 157.8 -> 137.3 ms), the one for 3 (80
+  // higher grids of at least 1.5 * 2^20 vertices (thick fronts: C3 157.8 -> 137.3 ms), the one for 3 (80
   // registers) otherwise, where cycles are short or fronts thin and the grid barriers dominate
   // (C2 1024^2, C4 fractal: 24.6 vs 31 ms).
   const char* bps = getenv("WCSP_BLOCKS_PER_SM");                   // A/B runs
-  h->big = opt.engine == WCSP_ENGINE_WHEEL && (bps ? atoi(bps) >= 4 : p->d >= 3 && N >= (1ull << 21));
+  // (lagged kernel, profiles/r02/ab_bps_lag.txt: 3-D from 1.5 * 2^20 vertices — P6-125, 1.95M: 13.0 ->
+  // 10.7 ms; P6-100, 1.0M: 7.07 vs 7.31 ms, P6-75 and P6-50 also faster with 3)
+  h->big = opt.engine == WCSP_ENGINE_WHEEL && (bps ? atoi(bps) >= 4 : p->d >= 3 && N >= (3ull << 19));
   int per_sm = 0;
   CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cycle_fn_d(p->d, opt.engine, h->big), THREADS,
                                                     sizeof(Smem)));

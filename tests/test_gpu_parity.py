@@ -533,7 +533,7 @@ def test_C5_full_size_one_gpu():
 @pytest.mark.parametrize("bps", ["3", "4"])
 def test_both_cycle_kernel_builds(bps, monkeypatch):
     """The persistent wheel kernel exists in two builds (4 resident blocks per SM,
-    64 registers, taken for 3-D grids >= 2^21 vertices; 3 blocks, 80 registers, otherwise).
+    64 registers, taken for 3-D grids >= 1.5 * 2^20 vertices; 3 blocks, 80 registers, otherwise).
     WCSP_BLOCKS_PER_SM forces either; both must give the oracle's outputs and tier 5's counters,
     on random small cases and on face-to-face cubes that span several treat rounds per block."""
     monkeypatch.setenv("WCSP_BLOCKS_PER_SM", bps)

@@ -260,7 +260,8 @@ Dev make_dev(const wcsp_handle* h) {
   // k_wheel_lag A/B: warp 1 waits for the neighbourhood beside warp 0's decision (C3 122.6 -> 122.9,
   // C2 85.3 -> 87.5, C3s 14.3 -> 14.1 ms; profiles/r02/ab_lag_par.txt): off
   s.lag_par = getenv("WCSP_LAG_PAR") ? atoi(getenv("WCSP_LAG_PAR")) != 0 : 0;
-  s.lag_pre = getenv("WCSP_LAG_PRE") ? atoi(getenv("WCSP_LAG_PRE")) != 0
+  // WCSP_LAG_PRE=2: before treat(c) only if every block's fire(c - 1) is already counted, else after
+  s.lag_pre = getenv("WCSP_LAG_PRE") ? atoi(getenv("WCSP_LAG_PRE"))
                                      : 8.0 * (double)h->N <= 4.0 * (double)std::max<long long>(h->l2_bytes, 1);
   // sparse cycles: about 64 triggered vertices per block (WCSP_LIST_MAX overrides, A/B runs)
   s.list_max = getenv("WCSP_LIST_MAX") ? strtoull(getenv("WCSP_LIST_MAX"), nullptr, 10)

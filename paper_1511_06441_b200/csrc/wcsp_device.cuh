@@ -228,7 +228,7 @@ struct Dev {
   unsigned long long* prog;        // [nblocks] treats completed (monotone per solve)
   int hyb_R;
   int hyb_prep;                    // run the fire's own-data prologue before the neighbourhood wait
-  int lag_pre;                     // k_wheel_lag A/B: decision c - 1 before treat(c) instead of after
+  int lag_pre;                     // k_wheel_lag: decision c - 1 before treat(c) (1), after (0), before if ready (2)
   int lag_par;                     // k_wheel_lag: that decision (warp 0) and the neighbourhood wait (warp 1) together
   // slab partition (multi-GPU / virtual slabs): local index + goff = global index
   unsigned goff;

@@ -1276,7 +1276,10 @@ __device__ void decide_lag(const Dev& s, LagState& L, bool writer) {
 
 // Take the decisions up to cycle `upto` (warp 0 waits for each cycle's fire count) and, if
 // wait_c > 0, wait for the neighbourhood's prog >= wait_c at the same time (warp 1).  False: abort.
-__device__ bool decide_upto(const Dev& s, Smem& sm, unsigned upto, unsigned long long wait_c = 0) {
+// nowait: take only the decisions whose fire counts are already complete (no polling; the rest
+// are taken by a later call).
+__device__ bool decide_upto(const Dev& s, Smem& sm, unsigned upto, unsigned long long wait_c = 0,
+                            bool nowait = false) {
   if (wait_c > 0 && threadIdx.x >= 32 && threadIdx.x < 64) {
     const unsigned ok = neigh_wait_warp(s, wait_c);
     if (threadIdx.x == 32) sm.flag2 = ok;
@@ -1289,6 +1292,7 @@ __device__ bool decide_upto(const Dev& s, Smem& sm, unsigned upto, unsigned long
       __syncwarp();
       const unsigned x = sm.lag.dn;
       if (x > upto || sm.lag.status != ST_RUNNING) break;
+      if (x > 0 && nowait && !__all_sync(0xFFFFFFFFu, ld_acquire_u32(&s.ctl->acc[x % NACC].nfire) >= G)) break;
       if (x > 0) {
         const unsigned long long t0 = globaltimer_ns();
         while (!__all_sync(0xFFFFFFFFu, ld_acquire_u32(&s.ctl->acc[x % NACC].nfire) >= G)) {
@@ -1357,7 +1361,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_lag(Dev s) {
       if (!decide_upto(s, sm, c)) return;
       if (sm.lag.status != ST_RUNNING) break;
     } else if (s.lag_pre) {        // decision c - 1 (warp 0) beside the wait for the neighbours' fire(c)
-      if (!decide_upto(s, sm, c - 1, s.lag_par ? 2ull * c + 1 : 0ull)) return;
+      if (!decide_upto(s, sm, c - 1, s.lag_par ? 2ull * c + 1 : 0ull, s.lag_pre == 2)) return;
       if (sm.lag.status != ST_RUNNING) break;
       if (!s.lag_par && !local_wait(s, sm, 2ull * c + 1)) return;
     } else if (!local_wait(s, sm, 2ull * c + 1)) return;
@@ -1371,7 +1375,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_wheel_lag(Dev s) {
     __syncthreads();
     phase_treat<D, true>(s, v, sm);                     // treat(c) with cycle c's view
     publish_treat(s, 2ull * c + 2);
-    if (!early && !s.lag_pre) {
+    if (!early && s.lag_pre != 1) {  // (lag_pre 2: only what the try before treat(c) left)
       if (!decide_upto(s, sm, c - 1)) return;
       if (sm.lag.status != ST_RUNNING) break;
     }

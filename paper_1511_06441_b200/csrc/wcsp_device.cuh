@@ -957,7 +957,8 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 // one per predicated lane (warp-aggregated).
 #ifndef WCSP_TREAT_EAGER
 #define WCSP_TREAT_EAGER 0         // 1: issue the neighbour loads together with Q's own (measured: no gain on C3)
-#endif
+#endif                             // 2: on 2-D grids only
+__host__ __device__ constexpr bool treat_eager(int d) { return WCSP_TREAT_EAGER == 1 || (WCSP_TREAT_EAGER == 2 && d == 2); }
 #ifndef WCSP_ROUND_SHARE
 #define WCSP_ROUND_SHARE 1         // the warps of a block share each treat round's vertices
 #endif
@@ -1055,15 +1056,13 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
 #endif
   const WRec<LW> wr = valid ? load_wt_cs<D>(s, q) : WRec<LW>{0, 0};
   unsigned long long swr[2 * D];
-#if WCSP_TREAT_EAGER
-  if constexpr (!PEER) {             // neighbours loaded with Q's own words: one memory round trip
+  if constexpr (!PEER && treat_eager(D)) {   // neighbours loaded with Q's own words: one round trip
 #pragma unroll
     for (int j = 0; j < 2 * D; ++j) {
       const unsigned u = q + s.off[j];
       swr[j] = valid && u < s.N ? s.sw[u] : 0xFFFFull;
     }
   }
-#endif
   LW w = 0;
   if constexpr (!WHEEL_ENGINE) w = valid ? __ldcg(reinterpret_cast<LW*>(s.res) + q) : (LW)0;
   const int lq = (int)(swq & 0xFFFFu);
@@ -1078,12 +1077,10 @@ __device__ __forceinline__ void treat_one(const Dev& s, const View& v, Smem& sm,
     const unsigned f1j = (unsigned)(wr.f1 >> (8 * j)) & 0xFFu;
     const unsigned f2j = s.minf ? 0u : (unsigned)(wr.f2 >> (8 * j)) & 0xFFu;
     const bool test = trig && f1j != 0 && lstar - (int)f2j > 0;
-#if WCSP_TREAT_EAGER
-    if constexpr (!PEER) {
+    if constexpr (!PEER && treat_eager(D)) {
       if (!test) swr[j] = 0xFFFFull;   // untested lanes read as "removed"
       continue;
     }
-#endif
     // L1-cached read: this phase never writes the temp half, the label half only moves to
     // max(L, temp) (benign), and the grid barrier before the phase invalidated L1
     if constexpr (PEER) {            // a neighbour in the next slab is read in its owner's memory

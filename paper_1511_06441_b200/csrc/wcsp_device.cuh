@@ -956,8 +956,8 @@ __device__ __forceinline__ bool lane_live(unsigned texp16, long long t) {
 // Stage events for the wheel (defined in wcsp_wheel.cuh): at a reserved staging slot, or
 // one per predicated lane (warp-aggregated).
 #ifndef WCSP_TREAT_EAGER
-#define WCSP_TREAT_EAGER 0         // 1: issue the neighbour loads together with Q's own (measured: no gain on C3)
-#endif                             // 2: on 2-D grids only
+#define WCSP_TREAT_EAGER 2         // 1: issue the neighbour loads together with Q's own; 2: on 2-D grids only
+#endif                             // (lagged kernel: C2 85.3 -> 83.4 ms, C3 +3.8 % with 1; ab_treat_lag*.txt)
 __host__ __device__ constexpr bool treat_eager(int d) { return WCSP_TREAT_EAGER == 1 || (WCSP_TREAT_EAGER == 2 && d == 2); }
 #ifndef WCSP_ROUND_SHARE
 #define WCSP_ROUND_SHARE 1         // the warps of a block share each treat round's vertices
@@ -967,7 +967,8 @@ __host__ __device__ constexpr bool treat_eager(int d) { return WCSP_TREAT_EAGER 
                                    //    measured on C3: treat +9 %, fire +64 % (interleaved runs) -- off
 #endif
 #ifndef WCSP_WIN_PREFETCH
-#define WCSP_WIN_PREFETCH 0        // 1: the next round's bitmap words load while this round is treated (no gain; off)
+#define WCSP_WIN_PREFETCH 1        // 1: the next round's bitmap words load while this round is treated (with TREAT_PF
+                                   // on the lagged kernel: C3 123.2 -> 121.85, C2 85.3 -> 83.6 ms; ab_treat_lag2.txt)
 #endif
 #ifndef WCSP_CLAIM
 #define WCSP_CLAIM 0               // 1: warps claim a round's batches dynamically (measured: C3 +0.6 %, C2 +1.8 %; off)
@@ -976,7 +977,7 @@ __host__ __device__ constexpr bool treat_eager(int d) { return WCSP_TREAT_EAGER 
 #define WCSP_NB_L2 0               // 1: the Step-4 neighbour words bypass L1 (A/B)
 #endif
 #ifndef WCSP_TREAT_PF
-#define WCSP_TREAT_PF 0            // 1: prefetch the next batch's state word (L2) and weight record (L1)
+#define WCSP_TREAT_PF 1            // 1: prefetch the next batch's state word (L2) and weight record (L1)
 #endif
 #ifndef WCSP_TREAT_AGG
 #define WCSP_TREAT_AGG 1           // one warp-scan staging reservation per treat batch (not one per lane direction)
